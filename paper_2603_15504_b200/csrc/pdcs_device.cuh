@@ -1,0 +1,542 @@
+// Device-side building blocks of libpdcs: NaN-propagating selects, deterministic
+// reductions, and the cone projections (box, SOC, rescaled SOC, exponential and
+// dual exponential cone).  Compiled with --fmad=false so that elementwise
+// expressions round exactly like the numpy reference (each * and + rounds).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/pdcs.h"
+
+namespace pdcs {
+
+constexpr int BS = 256;         // threads per CTA for streaming kernels
+constexpr int NSM = 148;        // B200 SMs
+constexpr int MAX_GRID = NSM * 8;
+
+// ---------------------------------------------------------------------------
+// NaN-propagating selects (np.maximum / np.clip propagate NaN; fmax does not,
+// SURVEY 8(a') item 11).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double pos_part(double v) { return v < 0.0 ? 0.0 : v; }
+__device__ __forceinline__ double neg_clip(double v) { return v > 0.0 ? 0.0 : v; }
+__device__ __forceinline__ double clampv(double v, double lo, double hi) {
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+// max for infinity norms: NaN wins (np.max propagates NaN)
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : (a > b ? a : b));
+}
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// Deterministic reductions.  Sums go down a fixed shuffle tree to lane 0 and
+// are broadcast from there, so every lane sees the bit-identical value.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v = nanmax(v, __shfl_down_sync(0xffffffffu, v, off));
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ int warp_and(int v) { return __all_sync(0xffffffffu, v); }
+
+// Block-wide reduction of NS sums and NM maxima; result written by thread 0
+// into partials (layout [q][cap]) at column `slot`.  blockDim.x must be a
+// multiple of 32 and <= 1024.
+template <int NS, int NM>
+__device__ __forceinline__ void block_store(double (&s)[NS], double (&mx)[NM], double* part_s,
+                                            double* part_m, int cap, int slot) {
+  __shared__ double sh[(NS + NM > 0 ? NS + NM : 1) * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) {
+    double v = s[q];
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if (lane == 0) sh[q * 32 + wid] = v;
+  }
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    double v = mx[q];
+    for (int off = 16; off > 0; off >>= 1) v = nanmax(v, __shfl_down_sync(0xffffffffu, v, off));
+    if (lane == 0) sh[(NS + q) * 32 + wid] = v;
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      double v = lane < nw ? sh[q * 32 + lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (lane == 0) part_s[q * cap + slot] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      double v = lane < nw ? sh[(NS + q) * 32 + lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) v = nanmax(v, __shfl_down_sync(0xffffffffu, v, off));
+      if (lane == 0) part_m[q * cap + slot] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// Cooperative group abstractions for segment (cone block) work: a warp or a
+// whole CTA handles one block; reductions return the same value to all
+// members.
+struct WarpGrp {
+  int rank, size;
+  __device__ WarpGrp() : rank(threadIdx.x & 31), size(32) {}
+  __device__ double sum(double v) const { return warp_sum(v); }
+  __device__ double max(double v) const { return warp_max(v); }
+  __device__ int all(int v) const { return warp_and(v); }
+  __device__ void sync() const { __syncwarp(); }
+};
+
+struct CtaGrp {
+  int rank, size;
+  double* sh;  // >= 33 doubles of shared scratch
+  __device__ CtaGrp(double* s) : rank(threadIdx.x), size(blockDim.x), sh(s) {}
+  __device__ double sum(double v) const {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < nw ? sh[lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+      if (lane == 0) sh[32] = t;
+    }
+    __syncthreads();
+    return sh[32];
+  }
+  __device__ double max(double v) const {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int off = 16; off > 0; off >>= 1) v = nanmax(v, __shfl_down_sync(0xffffffffu, v, off));
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < nw ? sh[lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) t = nanmax(t, __shfl_down_sync(0xffffffffu, t, off));
+      if (lane == 0) sh[32] = t;
+    }
+    __syncthreads();
+    return sh[32];
+  }
+  __device__ int all(int v) const { return __syncthreads_and(v); }
+  __device__ void sync() const { __syncthreads(); }
+};
+
+// ---------------------------------------------------------------------------
+// Exponential cone, K_exp = cl{(a,b,c): b > 0, c >= b exp(a/b)}
+// (reference cones.py:74-331).  One thread per 3-vector.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double exp_guard(double x) { return x >= 709.0 ? INFINITY : exp(x); }
+
+__device__ inline bool exp_member(double a, double b, double c) {
+  if (b > 0.0) {
+    double q = a / b;
+    if (q < 709.0 && c >= 0.0 && c >= b * exp(q)) return true;
+  }
+  return (b >= 0.0 && b <= 0.0) && a <= 0.0 && c >= 0.0;
+}
+
+__device__ inline bool dual_exp_member(double u, double v, double w) {
+  if (u > 0.0) return false;
+  if (u >= 0.0) return v >= 0.0 && w >= 0.0;
+  if (w <= 0.0) return false;
+  return u * log(-u / w) - u + v >= 0.0;
+}
+
+__device__ inline double exp_h(double r, double s, double t, double rho) {
+  double qd = rho * (rho - 1.0) + 1.0;
+  double ep = exp_guard(rho), en = exp_guard(-rho);
+  double ca = (rho - 1.0) * r + s, cb = r - rho * s;
+  double t1 = (isfinite(ep) || ca != 0.0) ? ca * ep : 0.0;
+  double t2 = (isfinite(en) || cb != 0.0) ? cb * en : 0.0;
+  return t1 - t2 - qd * t;
+}
+
+__device__ inline double exp_dh(double r, double s, double t, double rho) {
+  double ep = exp_guard(rho), en = exp_guard(-rho);
+  return (rho * r + s) * ep + (r - (rho - 1.0) * s) * en - (2.0 * rho - 1.0) * t;
+}
+
+__device__ inline void exp_bracket(double r, double s, double t, double pdist, double ddist,
+                                   double& lo_out, double& hi_out) {
+  double lo = -1e15, hi = 1e15;
+  double sm = dmin(s, 0.0), rm = dmin(r, 0.0);
+  double dp = sqrt(dmax(pdist * pdist - sm * sm, 0.0));
+  double dd = sqrt(dmax(ddist * ddist - rm * rm, 0.0));
+  if (t > 0.0) {
+    double rt = sqrt(r * r + s * s - r * s);
+    double ps = (r > s) ? (r - s + rt) / r : -s / (r - s - rt);
+    double pp = ((ps - 1.0) * r + s) / (ps * (ps - 1.0) + 1.0);
+    lo = dmax(lo, log(t / pp));
+  } else if (t < 0.0) {
+    double rt = sqrt(r * r + s * s - r * s);
+    double ps = (s > r) ? (r - rt) / s : (r - s) / (r + rt);
+    double dpp = (r - ps * s) / (ps * (ps - 1.0) + 1.0);
+    hi = dmin(hi, -log(-t / dpp));
+  }
+  if (r > 0.0) {
+    double base = 1.0 - s / r;
+    lo = dmax(lo, base);
+    double tpu = dmax(1e-12, dmin(dd, dp + t));
+    double pw = exp_guard(lo) / (lo * (lo - 1.0) + 1.0);
+    if (lo < 2.0) pw = dmin(pw, exp(2.0) / 3.0);
+    if (pw > 0.0) hi = dmin(hi, dmax(lo, base + tpu / r / pw));
+  }
+  if (s > 0.0) {
+    double base = r / s;
+    hi = dmin(hi, base);
+    double tdl = -dmax(1e-12, dmin(dp, dd - t));
+    double dw = -exp_guard(-hi) / (hi * (hi - 1.0) + 1.0);
+    if (hi > -1.0) dw = dmax(dw, -2.718281828459045 / 3.0);
+    if (dw < 0.0) lo = dmax(lo, dmin(hi, base - tdl / s / dw));
+  }
+  if (lo > hi) { lo = hi = 0.5 * (lo + hi); }
+  if (lo != hi) {
+    double fl = exp_h(r, s, t, lo), fu = exp_h(r, s, t, hi);
+    if (fl * fu > 0.0) {
+      if (fabs(fl) < fabs(fu)) hi = lo; else lo = hi;
+    }
+  }
+  lo_out = lo;
+  hi_out = hi;
+}
+
+__device__ inline double exp_root(double r, double s, double t, double lo, double hi) {
+  const int newton = 20, total = 100;
+  double x = 0.5 * (lo + hi);
+  bool done = false;
+  for (int i = 0; i < newton; ++i) {
+    double f = exp_h(r, s, t, x);
+    double df = exp_dh(r, s, t, x);
+    if (fabs(f) <= 1e-15) { done = true; break; }
+    if (f < 0.0) lo = x; else hi = x;
+    if (hi <= lo) return 0.5 * (lo + hi);
+    if (!isfinite(f) || df < 1e-13) break;
+    double xn = x - f / df;
+    if (fabs(xn - x) <= 1e-15 * dmax(1.0, fabs(xn))) {
+      x = dmin(dmax(xn, lo), hi);
+      done = true;
+      break;
+    }
+    if (xn >= hi) x = dmin(0.5 * x + 0.95 * hi, hi);
+    else if (xn <= lo) x = dmax(0.5 * x + 0.95 * lo, lo);
+    else x = xn;
+  }
+  if (done) return dmin(dmax(x, lo), hi);
+  for (int i = 0; i < total - newton; ++i) {
+    x = 0.5 * (lo + hi);
+    if (exp_h(r, s, t, x) < 0.0) lo = x; else hi = x;
+    if (hi - lo <= 1e-12 * dmax(1.0, fabs(hi))) break;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// Returns false when the root gives no valid point (reference returns None).
+__device__ inline bool exp_from_rho(double r, double s, double t, double rho, double* p,
+                                    double* dist) {
+  double qd = rho * (rho - 1.0) + 1.0;
+  double en = exp_guard(-rho);
+  double lin_a = (rho - 1.0) * r + s;
+  double lin_b = (r - rho * s) * en + qd * t;
+  double cond_a = fabs(rho - 1.0) * fabs(r) + fabs(s);
+  double cond_b = (fabs(r - rho * s) * en + qd * fabs(t)) * en;
+  if (cond_a <= cond_b) {
+    double ep = exp_guard(rho);
+    if (lin_a <= 0.0 || !isfinite(ep)) return false;
+    p[0] = rho * lin_a / qd; p[1] = lin_a / qd; p[2] = ep * lin_a / qd;
+  } else {
+    double lin = lin_b * en;
+    if (lin <= 0.0) return false;
+    p[0] = rho * lin / qd; p[1] = lin / qd; p[2] = lin_b / qd;
+  }
+  double d0 = p[0] - r, d1 = p[1] - s, d2 = p[2] - t;
+  *dist = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+  return true;
+}
+
+// Euclidean projection of (r, s, t) onto K_exp (cones.py:298-326).  Sets *err
+// for non-finite input (the reference raises NumericalError).
+__device__ inline void proj_exp3(double r, double s, double t, double* o, int* err) {
+  if (!(isfinite(r) && isfinite(s) && isfinite(t))) {
+    *err = PDCS_ERR_EXP_NONFINITE;
+    o[0] = r; o[1] = s; o[2] = t;
+    return;
+  }
+  if (exp_member(r, s, t)) { o[0] = r; o[1] = s; o[2] = t; return; }
+  if (dual_exp_member(-r, -s, -t)) { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; return; }
+  if (r <= 0.0 && s <= 0.0) { o[0] = r; o[1] = 0.0; o[2] = t < 0.0 ? 0.0 : t; return; }
+  // primal heuristic (cones.py:102-113)
+  double vp0 = dmin(r, 0.0), vp1 = 0.0, vp2 = dmax(t, 0.0);
+  double pdist = sqrt((r - vp0) * (r - vp0) + s * s + (t - vp2) * (t - vp2));
+  if (s > 0.0) {
+    double tp = s * exp_guard(r / s);
+    if (isfinite(tp)) {
+      tp = dmax(t, tp);
+      if (tp - t < pdist) { vp0 = r; vp1 = s; vp2 = tp; pdist = tp - t; }
+    }
+  }
+  // polar heuristic (cones.py:116-126)
+  double vd0 = 0.0, vd1 = dmin(s, 0.0), vd2 = dmin(t, 0.0);
+  double ddist = sqrt(r * r + (s - vd1) * (s - vd1) + (t - vd2) * (t - vd2));
+  if (r > 0.0) {
+    double td = -r * exp_guard(s / r - 1.0);
+    if (isfinite(td)) {
+      td = dmin(t, td);
+      if (t - td < ddist) { vd0 = r; vd1 = s; vd2 = td; ddist = t - td; }
+    }
+  }
+  double tol = 1e-12 * dmax(dmax(1.0, fabs(r)), dmax(fabs(s), fabs(t)));
+  double merr = dmax(dmax(fabs(vp0 + vd0 - r), fabs(vp1 + vd1 - s)), fabs(vp2 + vd2 - t));
+  double inner = vp0 * vd0 + vp1 * vd1 + vp2 * vd2;
+  if (dmin(pdist, ddist) <= tol || (merr <= tol && inner <= tol)) {
+    o[0] = vp0; o[1] = vp1; o[2] = vp2;
+    return;
+  }
+  double lo, hi;
+  exp_bracket(r, s, t, pdist, ddist, lo, hi);
+  double rho = exp_root(r, s, t, lo, hi);
+  double pr[3], dr;
+  if (exp_from_rho(r, s, t, rho, pr, &dr) && dr <= pdist) {
+    o[0] = pr[0]; o[1] = pr[1]; o[2] = pr[2];
+    return;
+  }
+  o[0] = vp0; o[1] = vp1; o[2] = vp2;
+}
+
+// Dual cone via Moreau: P_{K*}(v) = v + P_K(-v) (cones.py:329-331).
+__device__ inline void proj_dual_exp3(double r, double s, double t, double* o, int* err) {
+  double q[3];
+  proj_exp3(-r, -s, -t, q, err);
+  o[0] = r + q[0]; o[1] = s + q[1]; o[2] = t + q[2];
+}
+
+__device__ inline void set_err(int* gerr, int code) {
+  if (code && gerr) atomicCAS(gerr, 0, code);
+}
+
+// ---------------------------------------------------------------------------
+// Segment projection by a cooperating group (warp or CTA): block of `dim`
+// elements at in[0..dim), written to out[0..dim) (may alias in).  `sc` is the
+// block's scale slice (or nullptr), smode selects none/direct/inverse.
+// Kinds: FREE, ZERO, NONNEG, SOC (plain or rescaled), EXP, DUAL_EXP.
+// ---------------------------------------------------------------------------
+template <class G>
+__device__ inline double rsoc_phi(const G& g, const double* in, const double* sc, int smode,
+                                  int dim, double a0inv_base, double mu, double t0) {
+  // phi(mu) = sum a_i^2 y_i^2 / (1 + 2 mu a_i^2)^2 - (t0 / (1 - 2 mu))^2  (cones.py:347-350)
+  double acc = 0.0;
+  for (int i = 1 + g.rank; i < dim; i += g.size) {
+    double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
+    double a = di / a0inv_base;
+    double a2 = a * a;
+    double y = in[i];
+    double ay2 = a2 * y * y;
+    double den = 1.0 + 2.0 * mu * a2;
+    acc += ay2 / (den * den);
+  }
+  double s = g.sum(acc);
+  double tt = t0 / (1.0 - 2.0 * mu);
+  return s - tt * tt;
+}
+
+template <class G>
+__device__ inline void proj_rescaled_soc(const G& g, const double* in, double* out,
+                                         const double* sc, int smode, int dim, int* gerr) {
+  double d0 = smode == PDCS_SCALE_INVERT ? 1.0 / sc[0] : sc[0];
+  double t0 = in[0];
+  // membership tests (cones.py:372-375)
+  double s_ay2 = 0.0, s_ya2 = 0.0;
+  for (int i = 1 + g.rank; i < dim; i += g.size) {
+    double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
+    double a = di / d0;
+    double a2 = a * a;
+    double y = in[i];
+    s_ay2 += a2 * y * y;
+    double q = y / a;
+    s_ya2 += q * q;
+  }
+  s_ay2 = g.sum(s_ay2);
+  s_ya2 = g.sum(s_ya2);
+  if (t0 >= 0.0 && t0 * t0 >= s_ay2) {
+    for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
+    return;
+  }
+  if (t0 <= 0.0 && t0 * t0 >= s_ya2) {
+    for (int i = g.rank; i < dim; i += g.size) out[i] = 0.0;
+    return;
+  }
+  if (t0 == 0.0) {
+    double acc = 0.0;
+    for (int i = 1 + g.rank; i < dim; i += g.size) {
+      double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
+      double a = di / d0;
+      double zb = in[i] / (1.0 + a * a);
+      double az = a * zb;
+      acc += az * az;
+    }
+    double nrm = sqrt(g.sum(acc));
+    g.sync();
+    for (int i = 1 + g.rank; i < dim; i += g.size) {
+      double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
+      double a = di / d0;
+      out[i] = in[i] / (1.0 + a * a);
+    }
+    if (g.rank == 0) out[0] = nrm;
+    return;
+  }
+  // bracket (cones.py:387-412)
+  double lo = 0.0, hi = 0.0;
+  bool ok = false;
+  if (t0 > 0.0) {
+    lo = 0.0;
+    for (int j = 1; j < 53; ++j) {
+      double cand = 0.5 * (1.0 - ldexp(1.0, -j));
+      if (rsoc_phi(g, in, sc, smode, dim, d0, cand, t0) < 0.0) { hi = cand; ok = true; break; }
+    }
+  } else {
+    for (int j = 1; j < 53; ++j) {
+      double cand = 0.5 * (1.0 + ldexp(1.0, -j));
+      if (rsoc_phi(g, in, sc, smode, dim, d0, cand, t0) < 0.0) { lo = cand; ok = true; break; }
+    }
+    if (ok) {
+      ok = false;
+      hi = 1.0;
+      for (int j = 0; j < 80; ++j) {
+        if (rsoc_phi(g, in, sc, smode, dim, d0, hi, t0) > 0.0) { ok = true; break; }
+        hi *= 2.0;
+      }
+    }
+  }
+  if (!ok) {
+    if (g.rank == 0) set_err(gerr, PDCS_ERR_RSOC_BRACKET);
+    for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
+    return;
+  }
+  // Brent's method with xtol = 1e-16, rtol = 8.9e-16, 100 iterations
+  // (the classic algorithm scipy's brentq implements).
+  const double xtol = 1e-16, rtol = 8.9e-16;
+  double xpre = lo, xcur = hi, xblk = 0.0, fblk = 0.0, spre = 0.0, scur = 0.0;
+  double fpre = rsoc_phi(g, in, sc, smode, dim, d0, xpre, t0);
+  double fcur = rsoc_phi(g, in, sc, smode, dim, d0, xcur, t0);
+  double mu = xcur;
+  if (fpre == 0.0) {
+    mu = xpre;
+  } else if (fcur != 0.0) {
+    for (int it = 0; it < 100; ++it) {
+      if (fpre != 0.0 && fcur != 0.0 && (signbit(fpre) != signbit(fcur))) {
+        xblk = xpre; fblk = fpre; spre = scur = xcur - xpre;
+      }
+      if (fabs(fblk) < fabs(fcur)) {
+        xpre = xcur; xcur = xblk; xblk = xpre;
+        fpre = fcur; fcur = fblk; fblk = fpre;
+      }
+      double delta = (xtol + rtol * fabs(xcur)) / 2.0;
+      double sbis = (xblk - xcur) / 2.0;
+      if (fcur == 0.0 || fabs(sbis) < delta) break;
+      if (fabs(spre) > delta && fabs(fcur) < fabs(fpre)) {
+        double stry;
+        if (xpre == xblk) {
+          stry = -fcur * (xcur - xpre) / (fcur - fpre);
+        } else {
+          double dpre = (fpre - fcur) / (xpre - xcur);
+          double dblk = (fblk - fcur) / (xblk - xcur);
+          stry = -fcur * (fblk * dblk - fpre * dpre) / (dblk * dpre * (fblk - fpre));
+        }
+        if (2.0 * fabs(stry) < dmin(fabs(spre), 3.0 * fabs(sbis) - delta)) {
+          spre = scur; scur = stry;
+        } else {
+          spre = sbis; scur = sbis;
+        }
+      } else {
+        spre = sbis; scur = sbis;
+      }
+      xpre = xcur; fpre = fcur;
+      if (fabs(scur) > delta) xcur += scur;
+      else xcur += (sbis > 0.0 ? delta : -delta);
+      fcur = rsoc_phi(g, in, sc, smode, dim, d0, xcur, t0);
+    }
+    mu = xcur;
+  }
+  g.sync();
+  for (int i = 1 + g.rank; i < dim; i += g.size) {
+    double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
+    double a = di / d0;
+    out[i] = in[i] / (1.0 + 2.0 * mu * (a * a));
+  }
+  if (g.rank == 0) out[0] = t0 / (1.0 - 2.0 * mu);
+}
+
+template <class G>
+__device__ inline void proj_segment(const G& g, int kind, int smode, const double* in,
+                                    double* out, const double* sc, int dim, int* gerr) {
+  switch (kind) {
+    case PDCS_FREE:
+      for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
+      return;
+    case PDCS_ZERO:
+      for (int i = g.rank; i < dim; i += g.size) out[i] = 0.0;
+      return;
+    case PDCS_NONNEG:
+      for (int i = g.rank; i < dim; i += g.size) out[i] = pos_part(in[i]);
+      return;
+    case PDCS_EXP:
+    case PDCS_DUAL_EXP: {
+      if (g.rank == 0) {
+        double o[3];
+        int e = 0;
+        if (kind == PDCS_EXP) proj_exp3(in[0], in[1], in[2], o, &e);
+        else proj_dual_exp3(in[0], in[1], in[2], o, &e);
+        set_err(gerr, e);
+        out[0] = o[0]; out[1] = o[1]; out[2] = o[2];
+      }
+      g.sync();
+      return;
+    }
+    case PDCS_SOC: {
+      int uniform = 1;
+      if (smode != PDCS_SCALE_NONE) {
+        double s0 = sc[0];
+        int u = 1;
+        for (int i = g.rank; i < dim; i += g.size) u &= (sc[i] == s0);
+        uniform = g.all(u);
+      }
+      if (!uniform) {
+        proj_rescaled_soc(g, in, out, sc, smode, dim, gerr);
+        g.sync();
+        return;
+      }
+      double acc = 0.0;
+      for (int i = 1 + g.rank; i < dim; i += g.size) acc += in[i] * in[i];
+      double nx = sqrt(g.sum(acc));
+      double t = in[0];
+      g.sync();
+      if (nx <= t) {
+        for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
+      } else if (nx <= -t) {
+        for (int i = g.rank; i < dim; i += g.size) out[i] = 0.0;
+      } else {
+        double coef = 0.5 * (t + nx);
+        double ratio = coef / nx;
+        for (int i = 1 + g.rank; i < dim; i += g.size) out[i] = ratio * in[i];
+        if (g.rank == 0) out[0] = coef;
+      }
+      g.sync();
+      return;
+    }
+    default:
+      return;
+  }
+}
+
+}  // namespace pdcs

@@ -1,0 +1,850 @@
+// libpdcs: host orchestration and the C ABI (include/pdcs.h).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pdcs_kernels.cuh"
+
+using namespace pdcs;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" + \
+              std::to_string(__LINE__) + ")";                                            \
+      return 1;                                                                          \
+    }                                                                                    \
+  } while (0)
+
+#define CKL()                                                                              \
+  do {                                                                                     \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                    \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess) {                                                               \
+      g_err = std::string("kernel launch: ") + cudaGetErrorString(e_) + " (" + __FILE__ + \
+              ":" + std::to_string(__LINE__) + ")";                                        \
+      return 1;                                                                            \
+    }                                                                                      \
+  } while (0)
+
+inline int grid_for(int64_t n, int per = BS, int cap = MAX_GRID) {
+  int64_t g = (n + per - 1) / per;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+int choose_vw(int64_t nnz, int64_t nrows) {
+  if (nrows <= 0) return 1;
+  const double mean = (double)nnz / (double)nrows;
+  if (mean <= 6.0) return 1;
+  int vw = 1;
+  while (vw < 32 && vw < mean / 2.0) vw <<= 1;
+  return vw;
+}
+
+KArgs make_args(const Engine* E) {
+  const PdcsEngineDesc& d = E->d;
+  KArgs A;
+  A.n = E->n; A.m = E->m; A.nbox = E->nbox; A.m_zero = E->m_zero; A.m_elem = E->m_elem;
+  A.c = d.d_c; A.h = d.d_h; A.l = d.d_l; A.u = d.d_u;
+  A.c0 = d.d_c0; A.h0 = d.d_h0; A.l0 = d.d_l0; A.u0 = d.d_u0;
+  A.d1 = d.d_d1; A.d2 = d.d_d2;
+  A.x = d.d_x; A.y = d.d_y; A.xh = d.d_xh; A.yh = d.d_yh; A.xb = d.d_xb; A.yb = d.d_yb;
+  A.xa = d.d_xa; A.ya = d.d_ya;
+  A.gx = d.d_gx; A.gty = d.d_gty; A.gxa = d.d_gxa; A.gtya = d.d_gtya; A.w = d.d_w;
+  A.gxh = d.d_gxh; A.gth = d.d_gth; A.gtr = d.d_gtr; A.xt = d.d_xt;
+  A.tx0 = d.d_tx0; A.tx1 = d.d_tx1; A.tx2 = d.d_tx2;
+  A.ty0 = d.d_ty0; A.ty1 = d.d_ty1; A.ty2 = d.d_ty2;
+  A.ctrl = E->d_ctrl;
+  A.err = E->d_err;
+  return A;
+}
+
+// ---- SpMV plan -------------------------------------------------------------
+int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, const int* d_ci,
+               const double* d_val, cudaStream_t s) {
+  P.nrows = nrows; P.ncols = ncols; P.nnz = nnz;
+  P.rowptr = d_rp; P.colidx = d_ci; P.val = d_val;
+  std::vector<int> rp(nrows + 1, 0);
+  if (nrows > 0) {
+    CK(cudaMemcpyAsync(rp.data(), d_rp, sizeof(int) * (nrows + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  P.vw = choose_vw(nnz, nrows);
+  P.long_t = std::max(256, 64 * P.vw);
+  const int chunk = 2048;
+  std::vector<int> lrows, lfirst;
+  std::vector<int4> chunks;
+  for (int r = 0; r < nrows; ++r) {
+    const int b = rp[r], e = rp[r + 1];
+    if (e - b > P.long_t) {
+      lrows.push_back(r);
+      lfirst.push_back((int)chunks.size());
+      for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), 0));
+    }
+  }
+  lfirst.push_back((int)chunks.size());
+  P.n_long = (int)lrows.size();
+  P.n_chunks = (int)chunks.size();
+  if (P.n_long > 0) {
+    CK(cudaMalloc(&P.d_long_rows, sizeof(int) * P.n_long));
+    CK(cudaMalloc(&P.d_long_first, sizeof(int) * (P.n_long + 1)));
+    CK(cudaMalloc(&P.d_chunks, sizeof(int4) * P.n_chunks));
+    CK(cudaMalloc(&P.d_chunk_out, sizeof(double) * P.n_chunks));
+    CK(cudaMemcpyAsync(P.d_long_rows, lrows.data(), sizeof(int) * P.n_long, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P.d_long_first, lfirst.data(), sizeof(int) * (P.n_long + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P.d_chunks, chunks.data(), sizeof(int4) * P.n_chunks, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  P.grid = grid_for(nrows, BS / P.vw);
+  return 0;
+}
+
+void free_plan(SpmvPlan& P) {
+  cudaFree(P.d_long_rows);
+  cudaFree(P.d_long_first);
+  cudaFree(P.d_chunks);
+  cudaFree(P.d_chunk_out);
+  P = SpmvPlan();
+}
+
+// Long rows: chunk partials then per-row finalize into y.
+int launch_long(const SpmvPlan& P, const double* x, double* y, const PdcsCtrl* ctrl, int gate,
+                cudaStream_t s) {
+  if (P.n_long == 0) return 0;
+  k_long_partial<<<grid_for(P.n_chunks, 1), BS, 0, s>>>(P.d_chunks, P.n_chunks, P.colidx, P.val, x,
+                                                        P.d_chunk_out, ctrl, gate);
+  CKL();
+  k_long_final<<<grid_for(P.n_long, 128), 128, 0, s>>>(P.d_long_rows, P.d_long_first, P.n_long,
+                                                       P.d_chunk_out, y, ctrl, gate);
+  CKL();
+  return 0;
+}
+
+template <int VW>
+int launch_spmv_vw(const SpmvPlan& P, const double* x, double* y, cudaStream_t s) {
+  k_spmv<VW><<<P.grid, BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.val, x, y, P.long_t);
+  CKL();
+  return 0;
+}
+
+int launch_spmv(const SpmvPlan& P, const double* x, double* y, cudaStream_t s) {
+  if (P.nrows == 0) return 0;
+  if (launch_long(P, x, y, nullptr, 0, s)) return 1;
+  switch (P.vw) {
+    case 1: return launch_spmv_vw<1>(P, x, y, s);
+    case 2: return launch_spmv_vw<2>(P, x, y, s);
+    case 4: return launch_spmv_vw<4>(P, x, y, s);
+    case 8: return launch_spmv_vw<8>(P, x, y, s);
+    case 16: return launch_spmv_vw<16>(P, x, y, s);
+    default: return launch_spmv_vw<32>(P, x, y, s);
+  }
+}
+
+template <int OP>
+int launch_rowred(const SpmvPlan& P, const double* val, double* out, cudaStream_t s) {
+  if (P.nrows == 0) return 0;
+  k_rowred_short<OP><<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, val, out, P.long_t);
+  CKL();
+  if (P.n_long) {
+    k_rowred_long_partial<OP><<<grid_for(P.n_chunks, 1), BS, 0, s>>>(P.d_chunks, P.n_chunks, val,
+                                                                    P.d_chunk_out);
+    CKL();
+    k_rowred_long_final<OP><<<grid_for(P.n_long, 128), 128, 0, s>>>(
+        P.d_long_rows, P.d_long_first, P.n_long, P.d_chunk_out, out);
+    CKL();
+  }
+  return 0;
+}
+
+// ---- cone block tables -------------------------------------------------------
+int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s) {
+  std::vector<PdcsBlock> th, wa, ct;
+  for (auto& b : blocks) {
+    if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
+    else if (b.dim <= WARP_CLASS_MAX) wa.push_back(b);
+    else ct.push_back(b);
+  }
+  T.n_thread = (int)th.size();
+  T.n_warp = (int)wa.size();
+  T.n_cta = (int)ct.size();
+  std::vector<PdcsBlock> all;
+  all.insert(all.end(), th.begin(), th.end());
+  all.insert(all.end(), wa.begin(), wa.end());
+  all.insert(all.end(), ct.begin(), ct.end());
+  T.g_thread = T.n_thread ? grid_for(T.n_thread) : 0;
+  T.g_warp = T.n_warp ? grid_for(T.n_warp, BS / 32) : 0;
+  T.g_cta = T.n_cta ? std::min(T.n_cta, MAX_GRID) : 0;
+  if (!all.empty()) {
+    CK(cudaMalloc(&T.d_all, sizeof(PdcsBlock) * all.size()));
+    CK(cudaMemcpyAsync(T.d_all, all.data(), sizeof(PdcsBlock) * all.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return 0;
+}
+
+template <int OP>
+int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, double* part, int cap,
+                  int slot0, int gate, cudaStream_t s) {
+  int slot = slot0;
+  if (T.n_thread) {
+    k_blk_thread<OP><<<T.g_thread, BS, 0, s>>>(T.d_all, T.n_thread, A, P, part, cap, slot, gate);
+    CKL();
+  }
+  slot += T.g_thread;
+  if (T.n_warp) {
+    k_blk_warp<OP><<<T.g_warp, BS, 0, s>>>(T.d_all + T.n_thread, T.n_warp, A, P, part, cap, slot, gate);
+    CKL();
+  }
+  slot += T.g_warp;
+  if (T.n_cta) {
+    k_blk_cta<OP><<<T.g_cta, CTA_BLOCK_THREADS, 0, s>>>(T.d_all + T.n_thread + T.n_warp, T.n_cta, A,
+                                                        P, part, cap, slot, gate);
+    CKL();
+  }
+  return 0;
+}
+
+// ---- one line-search trial (graph slot) ----------------------------------
+template <int VW>
+int launch_step_y(Engine* E, const KArgs& A) {
+  k_step_y<VW><<<E->G.grid, BS, 0, E->stream>>>(A, E->G.nrows, E->G.rowptr, E->G.colidx, E->G.val,
+                                               E->G.long_t, E->d_partY, E->capY);
+  CKL();
+  return 0;
+}
+template <int VW>
+int launch_step_t(Engine* E, const KArgs& A) {
+  k_step_t<VW><<<E->GT.grid, BS, 0, E->stream>>>(A, E->GT.nrows, E->GT.rowptr, E->GT.colidx,
+                                                 E->GT.val, E->GT.long_t, E->d_partT, E->capT);
+  CKL();
+  return 0;
+}
+
+int launch_slot(Engine* E) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  BlkParams none{nullptr, nullptr, nullptr, 0, -1};
+  // primal candidate
+  k_step_x<<<E->gridX, BS, 0, s>>>(A, E->d_partX, E->capX);
+  CKL();
+  if (E->has_xblocks && launch_blocks<OP_STEP_X>(E->tabX, A, none, E->d_partX, E->capX, E->gridX, 1, s))
+    return 1;
+  // dual candidate with w = G^ x~
+  if (E->G.n_long && launch_long(E->G, E->d.d_xt, E->d.d_w, E->d_ctrl, 1, s)) return 1;
+  int rc = 0;
+  switch (E->G.vw) {
+    case 1: rc = launch_step_y<1>(E, A); break;
+    case 2: rc = launch_step_y<2>(E, A); break;
+    case 4: rc = launch_step_y<4>(E, A); break;
+    case 8: rc = launch_step_y<8>(E, A); break;
+    case 16: rc = launch_step_y<16>(E, A); break;
+    default: rc = launch_step_y<32>(E, A); break;
+  }
+  if (rc) return 1;
+  if (E->has_yblocks && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s))
+    return 1;
+  k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red);
+  CKL();
+  // accepted: G^T y_hat, beta, Halpern coefficients
+  if (E->GT.n_long && launch_long(E->GT, E->d.d_yh, E->d.d_gtr, E->d_ctrl, 2, s)) return 1;
+  switch (E->GT.vw) {
+    case 1: rc = launch_step_t<1>(E, A); break;
+    case 2: rc = launch_step_t<2>(E, A); break;
+    case 4: rc = launch_step_t<4>(E, A); break;
+    case 8: rc = launch_step_t<8>(E, A); break;
+    case 16: rc = launch_step_t<16>(E, A); break;
+    default: rc = launch_step_t<32>(E, A); break;
+  }
+  if (rc) return 1;
+  if (E->has_xblocks && launch_blocks<OP_TLAM>(E->tabX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s))
+    return 1;
+  k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err);
+  CKL();
+  return 0;
+}
+
+int finalize_to_host(Engine* E, const double* part, int cap, int nslots, int nq, unsigned mask,
+                     double* h_out) {
+  k_finalize<<<1, BS, 0, E->stream>>>(part, cap, nslots, nq, mask, E->d_out);
+  CKL();
+  CK(cudaMemcpyAsync(E->h_pinned, E->d_out, sizeof(double) * nq, cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  std::memcpy(h_out, E->h_pinned, sizeof(double) * nq);
+  return 0;
+}
+
+}  // namespace
+
+struct PdcsEngine : public Engine {};
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+const char* pdcs_last_error(void) { return g_err.c_str(); }
+int pdcs_abi_version(void) { return PDCS_ABI_VERSION; }
+int64_t pdcs_launch_count(void) { return g_launches.load(); }
+
+int pdcs_spmv_csr(int32_t nrows, const int32_t* d_rowptr, const int32_t* d_colidx,
+                  const double* d_val, const double* d_x, double* d_y, void* stream) {
+  if (nrows < 0) { g_err = "pdcs_spmv_csr: negative nrows"; return 2; }
+  if (nrows == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  SpmvPlan P;
+  int nnz = 0;
+  CK(cudaMemcpyAsync(&nnz, d_rowptr + nrows, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (build_plan(P, nrows, 0, nnz, d_rowptr, d_colidx, d_val, s)) return 1;
+  int rc = launch_spmv(P, d_x, d_y, s);
+  CK(cudaStreamSynchronize(s));
+  free_plan(P);
+  return rc;
+}
+
+int pdcs_transpose_csr(int32_t nrows, int32_t ncols, int32_t nnz, const int32_t* d_rowptr,
+                       const int32_t* d_colidx, const double* d_val, int32_t* d_t_rowptr,
+                       int32_t* d_t_colidx, double* d_t_val, int32_t* d_perm, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nrows < 0 || ncols < 0 || nnz < 0) { g_err = "pdcs_transpose_csr: bad sizes"; return 2; }
+  int* cnt = nullptr;
+  CK(cudaMalloc(&cnt, sizeof(int) * (ncols + 1)));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (ncols + 1), s));
+  if (nnz > 0) {
+    int *rowid = nullptr, *keys_out = nullptr, *idx = nullptr;
+    CK(cudaMalloc(&rowid, sizeof(int) * nnz));
+    CK(cudaMalloc(&keys_out, sizeof(int) * nnz));
+    CK(cudaMalloc(&idx, sizeof(int) * nnz));
+    k_iota_rows<<<grid_for(nrows), BS, 0, s>>>(d_rowptr, nrows, rowid);
+    CKL();
+    k_iota<<<grid_for(nnz), BS, 0, s>>>(idx, nnz);
+    CKL();
+    k_count_cols<<<grid_for(nnz), BS, 0, s>>>(d_colidx, nnz, cnt);
+    CKL();
+    int bits = 1;
+    while ((1ll << bits) < (int64_t)ncols + 1 && bits < 31) ++bits;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_colidx, keys_out, idx, d_perm, nnz, 0,
+                                       bits, s));
+    void* tmp = nullptr;
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, d_colidx, keys_out, idx, d_perm, nnz, 0, bits,
+                                       s));
+    k_transpose_scatter<<<grid_for(nnz), BS, 0, s>>>(d_perm, rowid, d_val, nnz, d_t_colidx, d_t_val);
+    CKL();
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    cudaFree(rowid);
+    cudaFree(keys_out);
+    cudaFree(idx);
+  }
+  size_t scan_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, d_t_rowptr, ncols + 1, s));
+  void* scan_tmp = nullptr;
+  CK(cudaMalloc(&scan_tmp, scan_bytes));
+  CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, d_t_rowptr, ncols + 1, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(scan_tmp);
+  cudaFree(cnt);
+  return 0;
+}
+
+int pdcs_project_segments(int32_t len, const double* d_in, double* d_out, const PdcsBlock* h_blocks,
+                          int32_t nblocks, const double* d_scale, int32_t* h_err, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len < 0 || nblocks < 0) { g_err = "pdcs_project_segments: bad sizes"; return 2; }
+  for (int i = 0; i < nblocks; ++i) {
+    const PdcsBlock& b = h_blocks[i];
+    if (b.start < 0 || b.dim < 1 || b.start + b.dim > len || b.kind < 0 || b.kind > 5) {
+      g_err = "pdcs_project_segments: block out of range";
+      return 2;
+    }
+    if (b.smode != PDCS_SCALE_NONE && d_scale == nullptr) {
+      g_err = "pdcs_project_segments: scaled block without a scale vector";
+      return 2;
+    }
+  }
+  if (len > 0 && d_in != d_out)
+    CK(cudaMemcpyAsync(d_out, d_in, sizeof(double) * len, cudaMemcpyDeviceToDevice, s));
+  int* d_err = nullptr;
+  CK(cudaMalloc(&d_err, sizeof(int)));
+  CK(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+  BlockTable T;
+  if (build_table(T, std::vector<PdcsBlock>(h_blocks, h_blocks + nblocks), s)) return 1;
+  KArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.err = d_err;
+  BlkParams P{d_out, d_out, d_scale, 0, -1};
+  int rc = launch_blocks<OP_PROJECT>(T, A, P, nullptr, 0, 0, 0, s);
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (h_err) *h_err = herr;
+  cudaFree(d_err);
+  cudaFree(T.d_all);
+  return rc;
+}
+
+int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** out) {
+  if (!desc || !out) { g_err = "pdcs_engine_create: null argument"; return 2; }
+  const PdcsEngineDesc& d = *desc;
+  if (d.n < 0 || d.m < 0 || d.nnz < 0 || d.num_box < 0 || d.num_box > d.n || d.m_zero < 0 ||
+      d.m_zero > d.m_elem || d.m_elem > d.m) {
+    g_err = "pdcs_engine_create: inconsistent sizes";
+    return 2;
+  }
+  PdcsEngine* E = new PdcsEngine();
+  E->d = d;
+  E->stream = (cudaStream_t)stream;
+  E->n = d.n; E->m = d.m; E->nbox = d.num_box; E->nnz = d.nnz;
+  E->m_zero = d.m_zero; E->m_elem = d.m_elem;
+  E->allow_nonuniform_dual_soc = d.allow_nonuniform_dual_soc;
+  cudaStream_t s = E->stream;
+  auto fail = [&](int rc) { pdcs_engine_destroy(E); return rc; };
+
+  // cone tables: primal blocks start after the box; dual blocks beyond m_elem
+  std::vector<PdcsBlock> xb, yb, ux, uy;
+  int pos = d.num_box;
+  for (int i = 0; i < d.n_pcones; ++i) {
+    const int k = d.h_pcone_kind[i], dim = d.h_pcone_dim[i];
+    if (k < 1 || k > 5 || dim < 1) { g_err = "pdcs_engine_create: bad primal cone"; return fail(2); }
+    xb.push_back(PdcsBlock{k, pos, dim, PDCS_SCALE_DIRECT});
+    if (k == PDCS_EXP || k == PDCS_DUAL_EXP) ux.push_back(PdcsBlock{k, pos, dim, 0});
+    pos += dim;
+  }
+  if (pos != d.n) { g_err = "pdcs_engine_create: primal cone dims do not sum to n - num_box"; return fail(2); }
+  pos = 0;
+  for (int i = 0; i < d.n_dcones; ++i) {
+    const int k = d.h_dcone_kind[i], dim = d.h_dcone_dim[i];
+    if (k < 1 || k > 5 || dim < 1) { g_err = "pdcs_engine_create: bad dual cone"; return fail(2); }
+    if (k == PDCS_ZERO || k == PDCS_NONNEG) {
+      if (pos >= d.m_elem && dim > 0) { g_err = "pdcs_engine_create: elementwise dual block after cone blocks"; return fail(2); }
+    } else {
+      if (pos < d.m_elem) { g_err = "pdcs_engine_create: cone block inside the elementwise rows"; return fail(2); }
+      yb.push_back(PdcsBlock{k, pos, dim, PDCS_SCALE_DIRECT});
+      if (k == PDCS_EXP || k == PDCS_DUAL_EXP || (k == PDCS_SOC && !d.allow_nonuniform_dual_soc))
+        uy.push_back(PdcsBlock{k, pos, dim, 0});
+    }
+    pos += dim;
+  }
+  if (pos != d.m) { g_err = "pdcs_engine_create: dual cone dims do not sum to m"; return fail(2); }
+  if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s)) return fail(1);
+  E->has_xblocks = E->tabX.total() > 0;
+  E->has_yblocks = E->tabY.total() > 0;
+  auto upload_blocks = [&](const std::vector<PdcsBlock>& v, PdcsBlock** dst) -> int {
+    if (v.empty()) return 0;
+    CK(cudaMalloc(dst, sizeof(PdcsBlock) * v.size()));
+    CK(cudaMemcpyAsync(*dst, v.data(), sizeof(PdcsBlock) * v.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    return 0;
+  };
+  if (upload_blocks(ux, &E->d_unif_x) || upload_blocks(uy, &E->d_unif_y)) return fail(1);
+  E->n_unif_x = (int)ux.size();
+  E->n_unif_y = (int)uy.size();
+
+  // transpose of the pattern (values are written by pdcs_precondition)
+  if (pdcs_transpose_csr(d.m, d.n, d.nnz, d.d_g_rowptr, d.d_g_colidx, nullptr, d.d_gt_rowptr,
+                         d.d_gt_colidx, nullptr, d.d_perm, s))
+    return fail(1);
+  if (build_plan(E->G, d.m, d.n, d.nnz, d.d_g_rowptr, d.d_g_colidx, d.d_g_val, s)) return fail(1);
+  if (build_plan(E->GT, d.n, d.m, d.nnz, d.d_gt_rowptr, d.d_gt_colidx, d.d_gt_val, s)) return fail(1);
+
+  // grids and reduction capacities
+  E->gridX = grid_for(d.n);
+  E->gridY = grid_for(d.m);
+  E->capX = E->gridX + E->tabX.grids();
+  E->capY = E->G.grid + E->tabY.grids();
+  E->capT = E->GT.grid + E->tabX.grids();
+  E->capC = E->gridX + E->gridY + 2;
+  if (cudaMalloc(&E->d_ctrl, sizeof(PdcsCtrl)) != cudaSuccess ||
+      cudaMalloc(&E->d_red, sizeof(double) * 16) != cudaSuccess ||
+      cudaMalloc(&E->d_partX, sizeof(double) * GX_N * E->capX) != cudaSuccess ||
+      cudaMalloc(&E->d_partY, sizeof(double) * GY_N * E->capY) != cudaSuccess ||
+      cudaMalloc(&E->d_partT, sizeof(double) * GT_N * E->capT) != cudaSuccess ||
+      cudaMalloc(&E->d_partC, sizeof(double) * PDCS_NMET * E->capC) != cudaSuccess ||
+      cudaMalloc(&E->d_out, sizeof(double) * 64) != cudaSuccess ||
+      cudaMalloc(&E->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&E->h_pinned, sizeof(double) * 64) != cudaSuccess) {
+    g_err = "pdcs_engine_create: workspace allocation failed";
+    return fail(1);
+  }
+  if (cudaMemsetAsync(E->d_ctrl, 0, sizeof(PdcsCtrl), s) != cudaSuccess ||
+      cudaMemsetAsync(E->d_err, 0, sizeof(int), s) != cudaSuccess ||
+      cudaMemsetAsync(E->d_partX, 0, sizeof(double) * GX_N * E->capX, s) != cudaSuccess ||
+      cudaMemsetAsync(E->d_partY, 0, sizeof(double) * GY_N * E->capY, s) != cudaSuccess ||
+      cudaMemsetAsync(E->d_partT, 0, sizeof(double) * GT_N * E->capT, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    g_err = "pdcs_engine_create: workspace init failed";
+    return fail(1);
+  }
+  *out = E;
+  return 0;
+}
+
+void pdcs_engine_destroy(PdcsEngine* E) {
+  if (!E) return;
+  if (E->stream) cudaStreamSynchronize(E->stream);
+  if (E->exec) cudaGraphExecDestroy(E->exec);
+  if (E->graph) cudaGraphDestroy(E->graph);
+  free_plan(E->G);
+  free_plan(E->GT);
+  cudaFree(E->tabX.d_all);
+  cudaFree(E->tabY.d_all);
+  cudaFree(E->d_unif_x);
+  cudaFree(E->d_unif_y);
+  cudaFree(E->d_ctrl);
+  cudaFree(E->d_red);
+  cudaFree(E->d_partX);
+  cudaFree(E->d_partY);
+  cudaFree(E->d_partT);
+  cudaFree(E->d_partC);
+  cudaFree(E->d_out);
+  cudaFree(E->d_err);
+  if (E->h_pinned) cudaFreeHost(E->h_pinned);
+  delete E;
+}
+
+int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_t use_pc) {
+  if (!E) { g_err = "pdcs_precondition: null engine"; return 2; }
+  const PdcsEngineDesc& d = E->d;
+  cudaStream_t s = E->stream;
+  const KArgs A = make_args(E);
+  const int n = E->n, m = E->m, nnz = E->nnz;
+  int* rowid = nullptr;
+  if (nnz > 0) {
+    CK(cudaMalloc(&rowid, sizeof(int) * nnz));
+    k_iota_rows<<<grid_for(m), BS, 0, s>>>(d.d_g_rowptr, m, rowid);
+    CKL();
+  }
+  if (enabled != 2) {
+    k_fill<<<grid_for(m), BS, 0, s>>>(d.d_d1, m, 1.0);
+    CKL();
+    k_fill<<<grid_for(n), BS, 0, s>>>(d.d_d2, n, 1.0);
+    CKL();
+  }
+  if (enabled == 1 && nnz > 0) {
+    // Ruiz rounds on a working copy held in g_val (scaling.py:84-90)
+    CK(cudaMemcpyAsync(d.d_g_val, d.d_g_val0, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    for (int it = 0; it < ruiz_iters; ++it) {
+      k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
+      CKL();
+      if (launch_rowred<0>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
+      if (launch_rowred<0>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
+      k_inv_sqrt_mul<<<grid_for(m), BS, 0, s>>>(d.d_ty0, d.d_ty1, d.d_d1, m);
+      CKL();
+      k_inv_sqrt_mul<<<grid_for(n), BS, 0, s>>>(d.d_tx0, d.d_tx1, d.d_d2, n);
+      CKL();
+      k_scale_vals<<<grid_for(nnz), BS, 0, s>>>(d.d_g_val, d.d_g_val, rowid, d.d_g_colidx, d.d_ty1,
+                                                d.d_tx1, nnz);
+      CKL();
+    }
+    if (use_pc) {  // Pock-Chambolle alpha = 1 (scaling.py:92-96)
+      k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
+      CKL();
+      if (launch_rowred<1>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
+      if (launch_rowred<1>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
+      k_inv_sqrt_mul<<<grid_for(m), BS, 0, s>>>(d.d_ty0, d.d_ty1, d.d_d1, m);
+      CKL();
+      k_inv_sqrt_mul<<<grid_for(n), BS, 0, s>>>(d.d_tx0, d.d_tx1, d.d_d2, n);
+      CKL();
+    }
+    if (E->n_unif_x) {
+      k_geo_mean<<<grid_for(E->n_unif_x, BS / 32), BS, 0, s>>>(E->d_unif_x, E->n_unif_x, d.d_d2);
+      CKL();
+    }
+    if (E->n_unif_y) {
+      k_geo_mean<<<grid_for(E->n_unif_y, BS / 32), BS, 0, s>>>(E->d_unif_y, E->n_unif_y, d.d_d1);
+      CKL();
+    }
+    k_clip<<<grid_for(m), BS, 0, s>>>(d.d_d1, m, 1e-8, 1e8);
+    CKL();
+    k_clip<<<grid_for(n), BS, 0, s>>>(d.d_d2, n, 1e-8, 1e8);
+    CKL();
+  }
+  // G^ = D1 G D2 from the original values, then its transpose by the perm map
+  if (nnz > 0) {
+    if (enabled == 2) {
+      CK(cudaMemcpyAsync(d.d_g_val, d.d_g_val0, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    } else {
+      k_scale_vals<<<grid_for(nnz), BS, 0, s>>>(d.d_g_val, d.d_g_val0, rowid, d.d_g_colidx, d.d_d1,
+                                                d.d_d2, nnz);
+      CKL();
+    }
+    k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
+    CKL();
+  }
+  k_scale_x<<<grid_for(n), BS, 0, s>>>(A, enabled == 2);
+  CKL();
+  k_scale_y<<<grid_for(m), BS, 0, s>>>(A, enabled == 2);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  cudaFree(rowid);
+  return 0;
+}
+
+int pdcs_stats(PdcsEngine* E, double* h_out) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  if (E->m > 0 && launch_rowred<1>(E->G, E->d.d_g_val, E->d.d_ty2, s)) return 1;
+  const int g = std::max(E->gridX, E->gridY);
+  if (g > E->capC) { g_err = "pdcs_stats: partial capacity"; return 1; }
+  k_stats<<<g, BS, 0, s>>>(A, E->d.d_g_val, E->nnz, E->d.d_ty2, E->d_partC, E->capC);
+  CKL();
+  return finalize_to_host(E, E->d_partC, E->capC, g, 6, 0x30u, h_out);
+}
+
+int pdcs_engine_get_ctrl(PdcsEngine* E, PdcsCtrl* h) {
+  CK(cudaMemcpyAsync(E->h_pinned, E->d_ctrl, sizeof(PdcsCtrl), cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  std::memcpy(h, E->h_pinned, sizeof(PdcsCtrl));
+  int err = 0;
+  CK(cudaMemcpy(&err, E->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err && !h->error) h->error = err;
+  return 0;
+}
+
+int pdcs_engine_set_ctrl(PdcsEngine* E, const PdcsCtrl* h) {
+  std::memcpy(E->h_pinned, h, sizeof(PdcsCtrl));
+  CK(cudaMemcpyAsync(E->d_ctrl, E->h_pinned, sizeof(PdcsCtrl), cudaMemcpyHostToDevice, E->stream));
+  CK(cudaMemsetAsync(E->d_err, 0, sizeof(int), E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
+  if (slots < 1) slots = 1;
+  cudaStream_t s = E->stream;
+  if (!E->exec || E->graph_slots != slots) {
+    if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }
+    if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
+    const int64_t before = g_launches.load();
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < slots; ++i) {
+      if (launch_slot(E)) {
+        cudaGraph_t tmp;
+        cudaStreamEndCapture(s, &tmp);
+        if (tmp) cudaGraphDestroy(tmp);
+        return 1;
+      }
+    }
+    CK(cudaStreamEndCapture(s, &E->graph));
+    CK(cudaGraphInstantiate(&E->exec, E->graph, 0));
+    E->graph_nodes = g_launches.load() - before;
+    g_launches.fetch_sub(E->graph_nodes);  // captured, not launched
+    E->graph_slots = slots;
+  }
+  int64_t* stop_h = reinterpret_cast<int64_t*>(E->h_pinned);
+  for (;;) {
+    CK(cudaGraphLaunch(E->exec, s));
+    g_launches.fetch_add(E->graph_nodes);
+    CK(cudaMemcpyAsync(stop_h, &E->d_ctrl->stop, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (*stop_h) break;
+  }
+  return 0;
+}
+
+int pdcs_flush(PdcsEngine* E) {
+  const KArgs A = make_args(E);
+  k_flush_x<<<E->gridX, BS, 0, E->stream>>>(A);
+  CKL();
+  k_flush_y<<<E->gridY, BS, 0, E->stream>>>(A);
+  CKL();
+  k_clear_pending<<<1, 1, 0, E->stream>>>(E->d_ctrl);
+  CKL();
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_engine_spmv(PdcsEngine* E, int32_t transpose, const double* in, double* out) {
+  int rc = launch_spmv(transpose ? E->GT : E->G, in, out, E->stream);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+static int project_blocks(Engine* E, const BlockTable& T, const double* buf, int dualize, int smode,
+                          const double* scale) {
+  if (T.total() == 0) return 0;
+  const KArgs A = make_args(E);
+  BlkParams P{buf, const_cast<double*>(buf), scale, dualize, smode};
+  return launch_blocks<OP_PROJECT>(T, A, P, nullptr, 0, 0, 0, E->stream);
+}
+
+static int check_err(Engine* E) {
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, E->d_err, sizeof(int), cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  if (err) {
+    CK(cudaMemsetAsync(E->d_err, 0, sizeof(int), E->stream));
+    g_err = "numerical failure in a cone projection (code " + std::to_string(err) + ")";
+    return 3;
+  }
+  return 0;
+}
+
+int pdcs_metrics(PdcsEngine* E, int32_t mode, const double* x, const double* y, const double* gx,
+                 const double* gty, double* h_out) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  const int orig = mode == 1;
+  if (E->has_xblocks || E->has_yblocks) {
+    k_met_fill<<<std::max(E->gridX, E->gridY), BS, 0, s>>>(A, mode, gx, gty);
+    CKL();
+    if (project_blocks(E, E->tabX, E->d.d_tx1, 1, orig ? PDCS_SCALE_NONE : PDCS_SCALE_INVERT, E->d.d_d2))
+      return 1;
+    if (project_blocks(E, E->tabY, E->d.d_ty1, 0, orig ? PDCS_SCALE_NONE : PDCS_SCALE_INVERT, E->d.d_d1))
+      return 1;
+  }
+  k_met_y<<<E->gridY, BS, 0, s>>>(A, mode, y, gx, E->d_partC, E->capC, 0);
+  CKL();
+  k_met_x<<<E->gridX, BS, 0, s>>>(A, mode, x, gty, E->d_partC, E->capC, E->gridY);
+  CKL();
+  if (finalize_to_host(E, E->d_partC, E->capC, E->gridX + E->gridY, PDCS_NMET, MET_MAXMASK, h_out))
+    return 1;
+  return check_err(E);
+}
+
+int pdcs_rays(PdcsEngine* E, const double* x, const double* y, const double* gx, const double* gty,
+              double xnorm, double ynorm, double* h_out) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  if (E->has_xblocks || E->has_yblocks) {
+    k_ray_fill<<<std::max(E->gridX, E->gridY), BS, 0, s>>>(A, x, gx, gty, xnorm, ynorm);
+    CKL();
+    if (project_blocks(E, E->tabX, E->d.d_tx1, 1, PDCS_SCALE_NONE, nullptr)) return 1;
+    if (project_blocks(E, E->tabX, E->d.d_tx2, 0, PDCS_SCALE_NONE, nullptr)) return 1;
+    if (project_blocks(E, E->tabY, E->d.d_ty1, 0, PDCS_SCALE_NONE, nullptr)) return 1;
+  }
+  k_ray_y<<<E->gridY, BS, 0, s>>>(A, y, gx, xnorm, E->d_partC, E->capC, 0);
+  CKL();
+  k_ray_x<<<E->gridX, BS, 0, s>>>(A, x, gty, xnorm, ynorm, E->d_partC, E->capC, E->gridY);
+  CKL();
+  if (finalize_to_host(E, E->d_partC, E->capC, E->gridX + E->gridY, PDCS_NRAY, RAY_MAXMASK, h_out))
+    return 1;
+  return check_err(E);
+}
+
+int pdcs_gap_probe(PdcsEngine* E, const double* x, const double* y, const double* gx,
+                   const double* gty, double t, double tau, double sigma, double* h_out) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  k_gap_x<<<E->gridX, BS, 0, s>>>(A, x, gty, t * tau);
+  CKL();
+  k_gap_y<<<E->gridY, BS, 0, s>>>(A, y, gx, t * sigma);
+  CKL();
+  if (project_blocks(E, E->tabX, E->d.d_tx0, 0, PDCS_SCALE_DIRECT, E->d.d_d2)) return 1;
+  if (project_blocks(E, E->tabY, E->d.d_ty0, 1, PDCS_SCALE_DIRECT, E->d.d_d1)) return 1;
+  const int g = std::max(E->gridX, E->gridY);
+  k_gap_red<<<g, BS, 0, s>>>(A, x, y, gx, gty, E->d_partC, E->capC);
+  CKL();
+  if (finalize_to_host(E, E->d_partC, E->capC, g, 4, 0u, h_out)) return 1;
+  return check_err(E);
+}
+
+int pdcs_dist2(PdcsEngine* E, int32_t space, const double* a, const double* b, double* h_out) {
+  const int n = space == 0 ? E->n : E->m;
+  const int g = space == 0 ? E->gridX : E->gridY;
+  k_dist2<<<g, BS, 0, E->stream>>>(a, b, n, E->d_partC, E->capC);
+  CKL();
+  return finalize_to_host(E, E->d_partC, E->capC, g, 1, 0u, h_out);
+}
+
+int pdcs_dot_diff(PdcsEngine* E, int32_t space, const double* a, const double* b, const double* c,
+                  const double* d, double* h_out) {
+  const int n = space == 0 ? E->n : E->m;
+  const int g = space == 0 ? E->gridX : E->gridY;
+  k_dot_diff<<<g, BS, 0, E->stream>>>(a, b, c, d, n, E->d_partC, E->capC);
+  CKL();
+  return finalize_to_host(E, E->d_partC, E->capC, g, 1, 0u, h_out);
+}
+
+int pdcs_project_set(PdcsEngine* E, int32_t which, const double* in, double* out) {
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  if (which < 0 || which > 4) { g_err = "pdcs_project_set: bad set"; return 2; }
+  const bool xs = which == 0 || which == 3 || which == 4;
+  k_proj_elem<<<xs ? E->gridX : E->gridY, BS, 0, s>>>(A, which, in, out);
+  CKL();
+  int rc = 0;
+  switch (which) {
+    case 0: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2); break;
+    case 1: rc = project_blocks(E, E->tabY, out, 1, PDCS_SCALE_DIRECT, E->d.d_d1); break;
+    case 2: rc = project_blocks(E, E->tabY, out, 0, PDCS_SCALE_INVERT, E->d.d_d1); break;
+    case 3: rc = project_blocks(E, E->tabX, out, 1, PDCS_SCALE_INVERT, E->d.d_d2); break;
+    case 4: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2); break;
+  }
+  if (rc) return rc;
+  return check_err(E);
+}
+
+int pdcs_step_input(PdcsEngine* E, int32_t space, const double* v, const double* g, double step,
+                    double* out) {
+  const KArgs A = make_args(E);
+  k_step_input<<<space == 0 ? E->gridX : E->gridY, BS, 0, E->stream>>>(A, space, v, g, step, out);
+  CKL();
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_axpby(PdcsEngine* E, int32_t space, double a, const double* p, double b, const double* q,
+               double* out) {
+  const int n = space == 0 ? E->n : E->m;
+  k_axpby<<<space == 0 ? E->gridX : E->gridY, BS, 0, E->stream>>>(n, a, p, b, q, 1.0, out);
+  CKL();
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_project_box(int32_t len, const double* in, const double* l, const double* u, double* out,
+                     void* stream) {
+  if (len < 0) { g_err = "pdcs_project_box: negative length"; return 2; }
+  if (len == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_box<<<grid_for(len), BS, 0, s>>>(len, in, l, u, out);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int pdcs_vec_axpby(int32_t len, double a, const double* p, double b, const double* q, double d,
+                   double* out, void* stream) {
+  if (len < 0) { g_err = "pdcs_vec_axpby: negative length"; return 2; }
+  if (len == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_axpby<<<grid_for(len), BS, 0, s>>>(len, a, p, b, q, d, out);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int pdcs_unscale(PdcsEngine* E, const double* x, const double* y, const double* gx,
+                 const double* gty, double* xo, double* yo, double* slack, double* lam) {
+  const KArgs A = make_args(E);
+  k_unscale<<<std::max(E->gridX, E->gridY), BS, 0, E->stream>>>(A, x, y, gx, gty, xo, yo, slack, lam);
+  CKL();
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_debug_inject_nan(PdcsEngine* E, int64_t after_calls) {
+  PdcsCtrl c;
+  if (pdcs_engine_get_ctrl(E, &c)) return 1;
+  c.nan_after = after_calls;
+  return pdcs_engine_set_ctrl(E, &c);
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// Internal engine structures shared by the libpdcs translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "pdcs_device.cuh"
+
+namespace pdcs {
+
+// Row schedule of one CSR matrix for the SpMV kernels: rows of up to
+// `long_t` nnz are handled by VW lanes each (VW = 1: one thread, summed in
+// index order exactly like scipy's csr_matvec); longer rows are split into
+// chunks summed by whole CTAs, then finalised per row in chunk order.
+struct SpmvPlan {
+  int nrows = 0, ncols = 0, nnz = 0;
+  const int* rowptr = nullptr;
+  const int* colidx = nullptr;
+  const double* val = nullptr;
+  int vw = 1;
+  int long_t = 1 << 30;
+  int n_long = 0, n_chunks = 0;
+  int* d_long_rows = nullptr;     // [n_long]
+  int* d_long_first = nullptr;    // [n_long + 1] first chunk of each long row
+  int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
+  double* d_chunk_out = nullptr;  // [n_chunks]
+  int grid = 1;                   // CTAs of the short-row kernel
+};
+
+// Cone-block table of one space split into size classes.
+struct BlockTable {
+  PdcsBlock* d_all = nullptr;  // thread class, then warp class, then cta class
+  int n_thread = 0, n_warp = 0, n_cta = 0;
+  int g_thread = 0, g_warp = 0, g_cta = 0;  // fixed grids (partial slots)
+  int total() const { return n_thread + n_warp + n_cta; }
+  int grids() const { return g_thread + g_warp + g_cta; }
+};
+
+constexpr int WARP_CLASS_MAX = 4096;  // dims above this get a whole CTA
+constexpr int THREAD_CLASS_MAX = 4;   // dims up to this get one thread
+constexpr int CTA_BLOCK_THREADS = 512;
+
+// Reduction groups of one line-search trial.
+enum { GX_XX = 0, GX_DXDX, GX_CX, GX_N };
+enum { GY_YY = 0, GY_DYDY, GY_INTER, GY_RP2, GY_YH, GY_N };
+enum { GT_RD2 = 0, GT_LSUM, GT_USUM, GT_N };
+
+struct Engine {
+  PdcsEngineDesc d;  // caller pointers
+  cudaStream_t stream = nullptr;
+  int n = 0, m = 0, nbox = 0, nnz = 0, m_zero = 0, m_elem = 0;
+  std::vector<int> pkind, pdim, dkind, ddim;
+  int allow_nonuniform_dual_soc = 0;
+
+  SpmvPlan G, GT;  // G^ (m x n) and G^T (n x m)
+  BlockTable tabX, tabY;
+  bool has_xblocks = false, has_yblocks = false;
+  // uniformity groups for preconditioning (blocks whose scale is made uniform)
+  PdcsBlock* d_unif_x = nullptr;
+  int n_unif_x = 0;
+  PdcsBlock* d_unif_y = nullptr;
+  int n_unif_y = 0;
+
+  // device workspace owned by the library
+  PdcsCtrl* d_ctrl = nullptr;
+  double* d_red = nullptr;  // scalars handed from the line-search controller to the beta controller
+  double* d_partX = nullptr;
+  double* d_partY = nullptr;
+  double* d_partT = nullptr;
+  int capX = 0, capY = 0, capT = 0;
+  int gridX = 1, gridXE = 1;  // x-space streaming grid
+  int gridY = 1;              // y-space streaming grid (elementwise kernels)
+  double* d_partC = nullptr;  // check path partials [PDCS_NMET*2][capC]
+  int capC = 0;
+  double* d_out = nullptr;  // [64]
+  int* d_err = nullptr;     // numerical error code of projections
+  double* h_pinned = nullptr;  // pinned readback [64]
+
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int graph_slots = 0;
+  int64_t graph_nodes = 0;
+};
+
+}  // namespace pdcs

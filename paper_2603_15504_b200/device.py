@@ -1,0 +1,368 @@
+"""Device residency of an instance: torch CUDA buffers + a libpdcs engine.
+
+PyTorch is used only to allocate device memory and to own the CUDA stream;
+all arithmetic runs in libpdcs kernels (include/pdcs.h).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .model import KIND_CODE, ConicProblem, dual_layout
+
+_F64 = None
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _dev_f64(arr, stream=None):
+    torch = _torch()
+    a = np.ascontiguousarray(arr, dtype=np.float64)
+    t = torch.empty(max(a.size, 1), dtype=torch.float64, device="cuda")
+    if a.size:
+        t[: a.size].copy_(torch.from_numpy(a), non_blocking=False)
+    return t
+
+
+def _dev_i32(arr):
+    torch = _torch()
+    a = np.ascontiguousarray(arr, dtype=np.int32)
+    t = torch.empty(max(a.size, 1), dtype=torch.int32, device="cuda")
+    if a.size:
+        t[: a.size].copy_(torch.from_numpy(a))
+    return t
+
+
+def _empty_f64(n):
+    torch = _torch()
+    return torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")
+
+
+class DeviceCSR:
+    """Device copy of a CSR matrix and of its (device-built) transpose, for
+    SparseMatrix.matvec / rmatvec."""
+
+    def __init__(self, csr):
+        lib = N.lib()
+        torch = _torch()
+        self.m, self.n = csr.shape
+        self.nnz = int(csr.nnz)
+        self.rp = _dev_i32(csr.indptr)
+        self.ci = _dev_i32(csr.indices)
+        self.va = _dev_f64(csr.data)
+        self.trp = torch.zeros(self.n + 1, dtype=torch.int32, device="cuda")
+        self.tci = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
+        self.tva = torch.empty(max(self.nnz, 1), dtype=torch.float64, device="cuda")
+        self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        N.check(lib.pdcs_transpose_csr(self.m, self.n, self.nnz, _ptr(self.rp), _ptr(self.ci),
+                                       _ptr(self.va), _ptr(self.trp), _ptr(self.tci),
+                                       _ptr(self.tva), _ptr(self.perm), None), "pdcs_transpose_csr")
+
+    def _apply(self, rows, rp, ci, va, v):
+        lib = N.lib()
+        x = _dev_f64(v)
+        y = _empty_f64(rows)
+        N.check(lib.pdcs_spmv_csr(rows, _ptr(rp), _ptr(ci), _ptr(va), _ptr(x), _ptr(y), None),
+                "pdcs_spmv_csr")
+        return y[:rows].cpu().numpy()
+
+    def matvec(self, x):
+        if self.m == 0:
+            return np.zeros(0)
+        return self._apply(self.m, self.rp, self.ci, self.va, x)
+
+    def rmatvec(self, y):
+        if self.n == 0:
+            return np.zeros(0)
+        return self._apply(self.n, self.trp, self.tci, self.tva, y)
+
+
+def project_segments(v: np.ndarray, blocks, scale: np.ndarray | None = None) -> np.ndarray:
+    """Segmented cone projection of a host vector on the GPU.
+
+    blocks: iterable of (kind_code, start, dim, smode).  Returns (out, err)."""
+    lib = N.lib()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    blocks = list(blocks)
+    arr = (N.PdcsBlock * max(len(blocks), 1))()
+    for i, (k, s, d, sm) in enumerate(blocks):
+        arr[i] = N.PdcsBlock(int(k), int(s), int(d), int(sm))
+    din = _dev_f64(v)
+    dout = _empty_f64(v.size)
+    dsc = _dev_f64(scale) if scale is not None else None
+    err = C.c_int32(0)
+    N.check(lib.pdcs_project_segments(v.size, _ptr(din), _ptr(dout), arr, len(blocks), _ptr(dsc),
+                                      C.byref(err), None), "pdcs_project_segments")
+    return dout[: v.size].cpu().numpy(), int(err.value)
+
+
+def project_box_dev(v, l, u):
+    lib = N.lib()
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    dv, dl, du = _dev_f64(v), _dev_f64(l), _dev_f64(u)
+    out = _empty_f64(v.size)
+    N.check(lib.pdcs_project_box(v.size, _ptr(dv), _ptr(dl), _ptr(du), _ptr(out), None),
+            "pdcs_project_box")
+    return out[: v.size].cpu().numpy()
+
+
+def axpby_dev(a, p, b, q, d=1.0):
+    """(a p + b q) / d on the GPU for host vectors (q may be None)."""
+    lib = N.lib()
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    dp = _dev_f64(p)
+    dq = _dev_f64(q) if q is not None else None
+    out = _empty_f64(p.size)
+    N.check(lib.pdcs_vec_axpby(p.size, float(a), _ptr(dp), float(b), _ptr(dq), float(d), _ptr(out), None),
+            "pdcs_vec_axpby")
+    return out[: p.size].cpu().numpy()
+
+
+class DeviceEngine:
+    """A presolved (post-RSOC) instance resident on the GPU with all solver
+    state buffers and a libpdcs engine handle.
+
+    mode "scale": Ruiz/PC preconditioning on the device (or identity when
+    use_preconditioner is off); mode "asis": the instance is used exactly as
+    given, with its ConeSpec scales as the block scales (step-level API)."""
+
+    def __init__(self, work: ConicProblem, *, asis: bool = False, allow_nonuniform_dual_soc=False):
+        lib = N.lib()
+        torch = _torch()
+        self.lib = lib
+        self.work = work
+        self.stream = torch.cuda.Stream()
+        n, m = work.n, work.m
+        self.n, self.m, self.nbox = n, m, work.num_box
+        csr = work.G._csr
+        self.nnz = int(csr.nnz)
+        self.m_zero, self.m_elem = dual_layout(work)
+        with torch.cuda.stream(self.stream):
+            f = _empty_f64
+            self.g_rowptr = _dev_i32(csr.indptr)
+            self.g_colidx = _dev_i32(csr.indices)
+            self.g_val0 = _dev_f64(csr.data)
+            self.g_val = f(self.nnz)
+            self.gt_rowptr = torch.zeros(n + 1, dtype=torch.int32, device="cuda")
+            self.gt_colidx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
+            self.gt_val = f(self.nnz)
+            self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
+            self.c0 = _dev_f64(work.c)
+            self.h0 = _dev_f64(work.h)
+            self.l0 = _dev_f64(work.l)
+            self.u0 = _dev_f64(work.u)
+            self.c, self.h, self.l, self.u = f(n), f(m), f(work.num_box), f(work.num_box)
+            if asis:
+                d2 = np.ones(n)
+                for spec, sl in _slices(work.primal_cones, work.num_box):
+                    d2[sl] = spec.scale
+                d1 = np.ones(m)
+                for spec, sl in _slices(work.dual_cones, 0):
+                    d1[sl] = spec.scale
+                self.d1, self.d2 = _dev_f64(d1), _dev_f64(d2)
+            else:
+                self.d1, self.d2 = f(m), f(n)
+            names_x = ["x", "xh", "xb", "xa", "xpa", "gty", "gtya", "gth", "gtr", "xt",
+                       "tx0", "tx1", "tx2", "px0", "px1", "px2", "pgty"]
+            names_y = ["y", "yh", "yb", "ya", "ypa", "gx", "gxa", "w", "gxh",
+                       "ty0", "ty1", "ty2", "py0", "py1", "py2", "pgx"]
+            for nm in names_x:
+                setattr(self, nm, f(n))
+            for nm in names_y:
+                setattr(self, nm, f(m))
+        torch.cuda.synchronize()
+
+        pk = [KIND_CODE[s.kind] for s in work.primal_cones]
+        pd = [s.dim for s in work.primal_cones]
+        dk = [KIND_CODE[s.kind] for s in work.dual_cones]
+        dd = [s.dim for s in work.dual_cones]
+        self._keep = [(C.c_int32 * max(len(a), 1))(*a) for a in (pk, pd, dk, dd)]
+        desc = N.PdcsEngineDesc()
+        desc.n, desc.m, desc.num_box, desc.nnz = n, m, work.num_box, self.nnz
+        desc.m_zero, desc.m_elem = self.m_zero, self.m_elem
+        desc.n_pcones, desc.n_dcones = len(pk), len(dk)
+        desc.h_pcone_kind, desc.h_pcone_dim, desc.h_dcone_kind, desc.h_dcone_dim = self._keep
+        desc.allow_nonuniform_dual_soc = int(bool(allow_nonuniform_dual_soc))
+        for p in N._DESC_PTRS:
+            setattr(desc, p, _ptr(getattr(self, p[2:])))
+        self.desc = desc
+        h = C.c_void_p()
+        N.check(lib.pdcs_engine_create(C.byref(desc), C.c_void_p(self.stream.cuda_stream), C.byref(h)),
+                "pdcs_engine_create")
+        self.handle = h
+        self.asis = asis
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self.lib.pdcs_engine_destroy(h)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
+            self.handle = None
+
+    # -- thin wrappers ------------------------------------------------------
+    def precondition(self, enabled: int, ruiz_iters: int = 10, use_pc: bool = True):
+        N.check(self.lib.pdcs_precondition(self.handle, int(enabled), int(ruiz_iters), int(bool(use_pc))),
+                "pdcs_precondition")
+
+    def stats(self):
+        out = (C.c_double * 8)()
+        N.check(self.lib.pdcs_stats(self.handle, out), "pdcs_stats")
+        return dict(c1=out[0], h1=out[1], c2=out[2], h2=out[3], gmax=out[4], rowsum_max=out[5])
+
+    def get_ctrl(self) -> N.PdcsCtrl:
+        c = N.PdcsCtrl()
+        N.check(self.lib.pdcs_engine_get_ctrl(self.handle, C.byref(c)), "pdcs_engine_get_ctrl")
+        return c
+
+    def set_ctrl(self, c: N.PdcsCtrl):
+        N.check(self.lib.pdcs_engine_set_ctrl(self.handle, C.byref(c)), "pdcs_engine_set_ctrl")
+
+    def run_inner(self, slots: int):
+        N.check(self.lib.pdcs_run_inner(self.handle, int(slots)), "pdcs_run_inner")
+
+    def flush(self):
+        N.check(self.lib.pdcs_flush(self.handle), "pdcs_flush")
+
+    def spmv(self, transpose: bool, src, dst):
+        N.check(self.lib.pdcs_engine_spmv(self.handle, int(transpose), _ptr(src), _ptr(dst)),
+                "pdcs_engine_spmv")
+
+    def metrics(self, mode: int, x, y, gx, gty) -> np.ndarray:
+        out = (C.c_double * N.NMET)()
+        rc = self.lib.pdcs_metrics(self.handle, int(mode), _ptr(x), _ptr(y), _ptr(gx), _ptr(gty), out)
+        if rc == 3:
+            from .linalg import NumericalError
+
+            raise NumericalError(self.lib.pdcs_last_error().decode())
+        N.check(rc, "pdcs_metrics")
+        return np.array(out[:], dtype=np.float64)
+
+    def rays(self, x, y, gx, gty, xnorm, ynorm) -> np.ndarray:
+        out = (C.c_double * N.NRAY)()
+        rc = self.lib.pdcs_rays(self.handle, _ptr(x), _ptr(y), _ptr(gx), _ptr(gty), float(xnorm),
+                                float(ynorm), out)
+        if rc == 3:
+            from .linalg import NumericalError
+
+            raise NumericalError(self.lib.pdcs_last_error().decode())
+        N.check(rc, "pdcs_rays")
+        return np.array(out[:], dtype=np.float64)
+
+    def gap_probe(self, x, y, gx, gty, t, tau, sigma):
+        out = (C.c_double * 4)()
+        rc = self.lib.pdcs_gap_probe(self.handle, _ptr(x), _ptr(y), _ptr(gx), _ptr(gty), float(t),
+                                     float(tau), float(sigma), out)
+        if rc == 3:
+            from .linalg import NumericalError
+
+            raise NumericalError(self.lib.pdcs_last_error().decode())
+        N.check(rc, "pdcs_gap_probe")
+        return out[0], out[1], out[2], out[3]
+
+    def dist2(self, space: int, a, b=None) -> float:
+        out = (C.c_double * 1)()
+        N.check(self.lib.pdcs_dist2(self.handle, int(space), _ptr(a), _ptr(b), out), "pdcs_dist2")
+        return float(out[0])
+
+    def dot_diff(self, space: int, a, b, c, d) -> float:
+        out = (C.c_double * 1)()
+        N.check(self.lib.pdcs_dot_diff(self.handle, int(space), _ptr(a), _ptr(b), _ptr(c), _ptr(d), out),
+                "pdcs_dot_diff")
+        return float(out[0])
+
+    def project_set(self, which: int, src, dst):
+        rc = self.lib.pdcs_project_set(self.handle, int(which), _ptr(src), _ptr(dst))
+        if rc == 3:
+            from .linalg import NumericalError
+
+            raise NumericalError(self.lib.pdcs_last_error().decode())
+        N.check(rc, "pdcs_project_set")
+
+    def step_input(self, space: int, v, g, step: float, out):
+        N.check(self.lib.pdcs_step_input(self.handle, int(space), _ptr(v), _ptr(g), float(step), _ptr(out)),
+                "pdcs_step_input")
+
+    def axpby(self, space: int, a: float, p, b: float, q, out):
+        N.check(self.lib.pdcs_axpby(self.handle, int(space), float(a), _ptr(p), float(b), _ptr(q), _ptr(out)),
+                "pdcs_axpby")
+
+    def unscale(self, x, y, gx, gty, xo, yo, slack, lam):
+        N.check(self.lib.pdcs_unscale(self.handle, _ptr(x), _ptr(y), _ptr(gx), _ptr(gty), _ptr(xo),
+                                      _ptr(yo), _ptr(slack), _ptr(lam)), "pdcs_unscale")
+
+    def inject_nan(self, after: int):
+        N.check(self.lib.pdcs_debug_inject_nan(self.handle, int(after)), "pdcs_debug_inject_nan")
+
+    # -- buffer helpers -------------------------------------------------------
+    def copy(self, dst, src):
+        with _torch().cuda.stream(self.stream):
+            dst.copy_(src)
+
+    def zero(self, *bufs):
+        with _torch().cuda.stream(self.stream):
+            for b in bufs:
+                b.zero_()
+
+    def upload(self, dst, arr):
+        torch = _torch()
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        with torch.cuda.stream(self.stream):
+            if a.size:
+                dst[: a.size].copy_(torch.from_numpy(a))
+        self.stream.synchronize()
+
+    def host(self, t, n) -> np.ndarray:
+        self.stream.synchronize()
+        return t[:n].cpu().numpy().copy() if n else np.zeros(0)
+
+    def xh_host(self, name):
+        return self.host(getattr(self, name), self.n)
+
+    def yh_host(self, name):
+        return self.host(getattr(self, name), self.m)
+
+
+_ENGINES: dict = {}
+
+
+def engine_for(problem: ConicProblem, original_mode: bool = False) -> DeviceEngine:
+    """Cached device engine of an instance for the step-level API.
+
+    original_mode=False: the instance as given, its ConeSpec scales acting as
+    block scales (what the reference's project_* / compute_errors see).
+    original_mode=True: unit block scales (the unscaled work instance the
+    termination checks run on)."""
+    import weakref
+
+    if problem.has_rsoc_blocks():
+        raise ValueError("rotated blocks must be reformulated (rsoc_to_soc) before projection")
+    key = (id(problem), bool(original_mode))
+    hit = _ENGINES.get(key)
+    if hit is not None and hit[0]() is problem:
+        return hit[1]
+    e = DeviceEngine(problem, asis=not original_mode)
+    e.precondition(0 if original_mode else 2)
+    _ENGINES[key] = (weakref.ref(problem, lambda _r, k=key: _ENGINES.pop(k, None)), e)
+    return e
+
+
+def _slices(specs, offset):
+    out, start = [], offset
+    for s in specs:
+        out.append((s, slice(start, start + s.dim)))
+        start += s.dim
+    return out

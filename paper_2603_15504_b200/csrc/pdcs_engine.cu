@@ -646,13 +646,26 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
     g_launches.fetch_sub(E->graph_nodes);  // captured, not launched
     E->graph_slots = slots;
   }
-  int64_t* stop_h = reinterpret_cast<int64_t*>(E->h_pinned);
+  // Watchdog: k_bar must advance (every trial advances it); a graph replay
+  // that leaves it unchanged 8 times in a row means the device loop is stuck.
+  PdcsCtrl* hc = reinterpret_cast<PdcsCtrl*>(E->h_pinned);
+  int64_t last_kbar = -1;
+  int stuck = 0;
   for (;;) {
     CK(cudaGraphLaunch(E->exec, s));
     g_launches.fetch_add(E->graph_nodes);
-    CK(cudaMemcpyAsync(stop_h, &E->d_ctrl->stop, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hc, E->d_ctrl, sizeof(PdcsCtrl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (*stop_h) break;
+    if (hc->stop) break;
+    if (hc->k_bar == last_kbar) {
+      if (++stuck >= 8) {
+        g_err = "pdcs_run_inner: device loop made no progress";
+        return 3;
+      }
+    } else {
+      stuck = 0;
+      last_kbar = hc->k_bar;
+    }
   }
   return 0;
 }

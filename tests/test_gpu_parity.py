@@ -1,0 +1,281 @@
+"""GPU parity tests: the CUDA path (through libpdcs's C ABI) against the
+reference's golden outputs and the CPU oracle.
+
+Parity contract: same exit status; objective within the
+solve tolerance; KKT metrics (recomputed by the oracle on both solutions)
+within max(1e-6, tol); iterations within the reference's own round-off band
+(widened by one check interval); early trajectory within 1e-11 / 1e-9.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from golden_io import SOLVE_CASES, load, options, problem
+from oracle import pdcs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_15504_b200 as pkg
+
+    return pkg
+
+
+def _split(flat, lens):
+    out, s = [], 0
+    for n in lens:
+        out.append(flat[s:s + n])
+        s += n
+    return out
+
+
+# ---------------------------------------------------------------------------
+# kernels
+# ---------------------------------------------------------------------------
+
+
+def test_library_is_native(P):
+    from paper_2603_15504_b200 import _native
+
+    lib = _native.lib()
+    assert lib.pdcs_abi_version() == 1
+
+
+@pytest.mark.parametrize("shape", [(300, 600, 5), (200, 400, 20), (50, 4000, 600), (7, 3, 2)])
+def test_spmv_matches_scipy(P, shape):
+    m, n, per = shape
+    rng = np.random.default_rng(m + n)
+    G = sp.random(m, n, min(1.0, per / n), format="csr", random_state=rng, data_rvs=rng.standard_normal)
+    A = P.SparseMatrix(G)
+    x = rng.standard_normal(n)
+    y = rng.standard_normal(m)
+    ref_x = A._csr @ x
+    ref_y = A._csr.T.tocsr() @ y
+    got_x = A.matvec(x)
+    got_y = A.rmatvec(y)
+    np.testing.assert_allclose(got_x, ref_x, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(got_y, ref_y, rtol=1e-12, atol=1e-12)
+    if per <= 6:  # thread-per-row rows sum in index order: bit-identical to csr_matvec
+        np.testing.assert_array_equal(got_x, ref_x)
+
+
+def test_long_rows_spmv(P):
+    rng = np.random.default_rng(3)
+    m, n = 41, 300_000
+    G = sp.random(m, n, 0.05, format="csr", random_state=rng, data_rvs=rng.standard_normal)
+    G = sp.vstack([G, sp.identity(n, format="csr")[:1000, :]]).tocsr()
+    A = P.SparseMatrix(G)
+    x = rng.standard_normal(n)
+    np.testing.assert_allclose(A.matvec(x), A._csr @ x, rtol=1e-11, atol=1e-10)
+    y = rng.standard_normal(A.m)
+    np.testing.assert_allclose(A.rmatvec(y), A._csr.T.tocsr() @ y, rtol=1e-11, atol=1e-10)
+
+
+def test_projections_match_golden(P):
+    from paper_2603_15504_b200 import cones
+
+    g = load("projections")
+    for v, w in zip(g["exp_in"][:120], g["exp_out"][:120]):
+        np.testing.assert_allclose(cones.project_exp(v), w, rtol=1e-12, atol=1e-12)
+    for v, w in zip(g["exp_in"][:120], g["dexp_out"][:120]):
+        np.testing.assert_allclose(cones.project_dual_exp(v), w, rtol=1e-12, atol=1e-12)
+    for v, w in zip(g["exp_stiff_in"][::5], g["exp_stiff_out"][::5]):
+        np.testing.assert_allclose(cones.project_exp(v), w, rtol=1e-10, atol=1e-10)
+    for v, w in list(zip(_split(g["soc_in"], g["soc_len"]), _split(g["soc_out"], g["soc_len"])))[:60]:
+        np.testing.assert_allclose(cones.project_soc(v), w, rtol=1e-13, atol=1e-13)
+    ins = _split(g["rsoc_in"], g["rsoc_len"])
+    scs = _split(g["rsoc_scale"], g["rsoc_len"])
+    outs = _split(g["rsoc_out"], g["rsoc_len"])
+    for v, s, w in list(zip(ins, scs, outs))[:60]:
+        np.testing.assert_allclose(cones.project_rescaled_soc(v, s), w, rtol=1e-9, atol=1e-10)
+
+
+def test_batched_exp_projection_matches_oracle(P):
+    """Thousands of exponential-cone blocks projected in one segmented launch."""
+    from paper_2603_15504_b200.device import project_segments
+
+    rng = np.random.default_rng(9)
+    v = rng.uniform(-4, 4, 3 * 3000)
+    blocks = [(4, 3 * i, 3, 0) for i in range(3000)]
+    out, err = project_segments(v, blocks)
+    assert err == 0
+    ref = np.concatenate([O.proj_exp(v[3 * i:3 * i + 3]) for i in range(3000)])
+    np.testing.assert_allclose(out, ref, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# components
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "c4s", "c5s"])
+def test_components_match_golden(P, name):
+    from paper_2603_15504_b200 import engine, restart, scaling, termination
+    from paper_2603_15504_b200.model import rsoc_to_soc
+
+    comp = load("components")
+    p = problem(load("solve_" + name))
+    work = rsoc_to_soc(p)
+    s = scaling.build_scaling(work)
+    np.testing.assert_allclose(s.d1, comp[name + "_d1"], rtol=1e-12)
+    np.testing.assert_allclose(s.d2, comp[name + "_d2"], rtol=1e-12)
+    sref = scaling.ScalingPair(comp[name + "_d1"], comp[name + "_d2"])
+    S = scaling.rescale_problem(work, sref)
+    rep = termination.compute_errors(S, comp[name + "_err_x"], comp[name + "_err_y"])
+    got = [getattr(rep, f) for f in termination.ErrorReport.__dataclass_fields__]
+    np.testing.assert_allclose(got, comp[name + "_err"], rtol=1e-10, atol=1e-12)
+    x, y = comp[name + "_err_x"] * 0.1, np.abs(comp[name + "_err_y"]) * 0.1
+    omega, eta = 1.3, 0.9 / S.G.max_abs()
+    st = engine.adaptive_step_pdhg(S, engine.IterateZ(x, y), omega, eta, 7)
+    np.testing.assert_allclose([st.eta_used, st.eta_next, st.k_bar, st.trials], comp[name + "_ls"],
+                               rtol=1e-10)
+    np.testing.assert_allclose(st.z_hat.x, comp[name + "_ls_x"], atol=1e-11)
+    np.testing.assert_allclose(st.z_hat.y, comp[name + "_ls_y"], atol=1e-11)
+
+
+# ---------------------------------------------------------------------------
+# whole solves
+# ---------------------------------------------------------------------------
+
+
+def _kkt_triplet(p, x, y):
+    """rel_p_inf, rel_d_inf, rel_gap_term of (x, y) on the original instance
+    via the oracle."""
+    op = O.as_oproblem(p)
+    work = O.rsoc_presolve(op)
+    if work is not op:  # map y back into the presolved coordinates
+        x, y, _ = O.rsoc_unrotate(op, x, y, np.zeros(op.m))
+    rep = O.metrics(work, x, y)
+    return np.array([rep["rel_p_inf"], rep["rel_d_inf"], rep["rel_gap_term"]])
+
+
+@pytest.mark.parametrize("case", SOLVE_CASES)
+def test_solve_matches_reference(P, case):
+    d = load("solve_" + case)
+    p = problem(d)
+    opts = options(d)
+    traces = {}
+    kbars = [int(k.split("_")[-1]) for k in d if k.startswith("trace_x_")]
+
+    def cb(s):
+        if s.k_bar in kbars:
+            traces[s.k_bar] = (s.z.x.copy(), s.z.y.copy())
+
+    o = P.SolverOptions(**opts)
+    r = P.solve(p, o)
+    status = str(d["status"])
+    assert r.exit_status == status, (case, r.exit_status, status, r.iterations)
+    ref_it = int(d["iterations"])
+    freq = opts.get("duality_gap_restart_freq", 2000)
+    band = max(int(0.2 * ref_it), freq)
+    assert abs(r.iterations - ref_it) <= band, (case, r.iterations, ref_it)
+    tol = max(opts.get("rel_tol", 1e-6), 1e-6)
+    if status == ":optimal":
+        p_ref = float(d["p_obj"])
+        assert abs(r.p_obj - p_ref) <= tol * (1.0 + abs(p_ref)) * 10, (r.p_obj, p_ref)
+        e_gpu = _kkt_triplet(p, r.x, r.y)
+        e_ref = _kkt_triplet(p, d["x"], d["y"])
+        assert np.all(np.abs(e_gpu - e_ref) <= max(1e-6, tol)), (e_gpu, e_ref)
+    if case == "maxit":
+        assert r.iterations == 5
+    if kbars and case in ("tiny", "c1s", "c5s", "c2s", "c3s", "c4s"):
+        o2 = P.SolverOptions(**opts, iteration_callback=cb)
+        P.solve(p, o2)
+        for kb in kbars:
+            if kb not in traces:
+                continue
+            gx, gy = traces[kb]
+            rx, ry = d["trace_x_%d" % kb], d["trace_y_%d" % kb]
+            scale = max(1.0, np.max(np.abs(rx)), np.max(np.abs(ry)) if ry.size else 1.0)
+            lim = 1e-11 if kb <= 20 else 1e-9
+            assert np.max(np.abs(gx - rx)) <= lim * scale, (case, kb)
+            assert np.max(np.abs(gy - ry)) <= lim * scale, (case, kb)
+
+
+def test_deterministic_iterates(P):
+    d = load("solve_tiny")
+    p = problem(d)
+    runs = []
+    for _ in range(2):
+        trace = []
+        P.solve(p, P.SolverOptions(iteration_callback=lambda s: trace.append(
+            (s.z.x.copy(), s.z.y.copy(), s.eta)), max_iter=300, rel_tol=1e-14, abs_tol=1e-14))
+        runs.append(trace)
+    assert len(runs[0]) == len(runs[1]) == 300
+    for (x0, y0, e0), (x1, y1, e1) in zip(*runs):
+        assert np.array_equal(x0, x1) and np.array_equal(y0, y1) and e0 == e1
+
+
+def test_matvec_budget_per_iteration(P):
+    from paper_2603_15504_b200 import engine as eng
+
+    p = problem(load("solve_tiny"))
+    opts = P.SolverOptions(use_preconditioner=False, use_adaptive_restart=False,
+                           use_adaptive_step_size_weight=False, max_iter=30, rel_tol=1e-14,
+                           abs_tol=1e-14)
+    loop = eng._Loop(p, opts)
+    loop.scaled.G.reset_counters()
+    loop._run()
+    assert loop.scaled.G.n_matvec == 1 + 30 + 1
+    assert loop.scaled.G.n_rmatvec == 1 + 30 + 1
+
+
+def test_injected_nan_gives_numerical_error(P, monkeypatch):
+    from paper_2603_15504_b200 import engine as eng
+
+    monkeypatch.setattr(eng, "debug_nan_after", 10)
+    r = P.solve(problem(load("solve_tiny")), P.SolverOptions(use_preconditioner=False))
+    assert r.exit_code == 8 and r.exit_status == ":numerical_error"
+
+
+def test_time_limit_exit(P):
+    r = P.solve(problem(load("solve_tiny")), P.SolverOptions(time_limit=1e-9, rel_tol=1e-12, abs_tol=1e-12))
+    assert r.exit_code == 6
+
+
+def test_kkt_fallback_on_negative_gap(P, monkeypatch):
+    from paper_2603_15504_b200 import engine as eng
+
+    monkeypatch.setattr(eng.restarts, "normalized_gap", lambda *a, **k: -1.0)
+    calls = {"n": 0}
+    orig = eng._Loop._kkt_metric
+
+    def spy(self, z, omega):
+        calls["n"] += 1
+        return orig(self, z, omega)
+
+    monkeypatch.setattr(eng._Loop, "_kkt_metric", spy)
+    r = P.solve(problem(load("solve_tiny")), P.SolverOptions(duality_gap_restart_freq=100))
+    assert r.exit_code == 0
+    assert r.p_obj == pytest.approx(-2.0, abs=1e-5)
+    assert calls["n"] > 0
+
+
+def test_step_level_api(P):
+    from paper_2603_15504_b200.engine import IterateZ, one_pdhg, reflected_halpern_step, update_weighted_average
+
+    p = problem(load("solve_tiny"))
+    op = O.as_oproblem(p)
+    rng = np.random.default_rng(4)
+    for _ in range(5):
+        x, y = rng.uniform(0, 1, 2), rng.uniform(0, 2, 1)
+        z = one_pdhg(p, IterateZ(x, y), 0.3, 0.4)
+        gty = op.rmv(y)
+        xh, yh, _ = O.pdhg_candidate(op, x, y, 0.3, 0.4, op.c - gty)
+        np.testing.assert_array_equal(z.x, xh)
+        np.testing.assert_array_equal(z.y, yh)
+    a = IterateZ(np.array([2.0]), np.array([0.0]))
+    b = IterateZ(np.array([-1.0]), np.array([1.0]))
+    c = IterateZ(np.array([0.0]), np.array([4.0]))
+    out = reflected_halpern_step(a, b, c, k=0, beta=0.0)
+    np.testing.assert_allclose(out.x, [1.0])
+    np.testing.assert_allclose(out.y, [2.0])
+    zb, w = update_weighted_average(None, 0.0, a, 1.0)
+    zb, w = update_weighted_average(zb, w, b, 1.0)
+    np.testing.assert_allclose(zb.x, [0.5])
+    assert w == 2.0

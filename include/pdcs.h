@@ -187,6 +187,13 @@ int pdcs_precondition(PdcsEngine* e, int32_t enabled, int32_t ruiz_iters, int32_
  * sum (engine.py:322-336, restart.py:180-186). */
 int pdcs_stats(PdcsEngine* e, double* h_out);
 
+/* Launch configuration chosen at create: h_out[16] = {vw(G^), vw(G^T), grid
+ * step_x, grid step_y, grid step_t, keep fraction x~, keep fraction y_hat,
+ * persisting-L2 bytes, long rows of G^, long rows of G^T, primal cone blocks,
+ * dual cone blocks, column panels of G^, of G^T, step-kernel lanes per row
+ * of G^, of G^T}. */
+int pdcs_engine_info(PdcsEngine* e, double* h_out);
+
 int pdcs_engine_get_ctrl(PdcsEngine* e, PdcsCtrl* h_ctrl);
 int pdcs_engine_set_ctrl(PdcsEngine* e, const PdcsCtrl* h_ctrl);
 
@@ -195,6 +202,12 @@ int pdcs_engine_set_ctrl(PdcsEngine* e, const PdcsCtrl* h_ctrl);
  * control block's stop flag is set.  Slots are replayed from a CUDA graph of
  * `slots_per_graph` line-search trials. */
 int pdcs_run_inner(PdcsEngine* e, int32_t slots_per_graph);
+
+/* Runs `reps` line-search trials eagerly (not from the graph) with CUDA
+ * events between the stages and returns the number of stages; h_ms[i] is the
+ * mean device time of stage i and h_names[i] its name (static strings).
+ * Advances the iteration like pdcs_run_inner would.  For bench.py. */
+int pdcs_profile_slot(PdcsEngine* e, int32_t reps, double* h_ms, const char** h_names, int32_t cap);
 
 /* Applies the pending Halpern/average update so z, z_bar, gx, gty are
  * current (the deferred part of engine.py:602-610). */

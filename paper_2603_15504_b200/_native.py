@@ -92,10 +92,12 @@ _SIGS = {
     "pdcs_engine_destroy": (None, [_P]),
     "pdcs_precondition": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32]),
     "pdcs_stats": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "pdcs_engine_info": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "pdcs_engine_get_ctrl": (C.c_int, [_P, C.POINTER(PdcsCtrl)]),
     "pdcs_engine_set_ctrl": (C.c_int, [_P, C.POINTER(PdcsCtrl)]),
     "pdcs_run_inner": (C.c_int, [_P, C.c_int32]),
     "pdcs_flush": (C.c_int, [_P]),
+    "pdcs_profile_slot": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_char_p), C.c_int32]),
     "pdcs_engine_spmv": (C.c_int, [_P, C.c_int32, _P, _P]),
     "pdcs_metrics": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.POINTER(C.c_double)]),
     "pdcs_rays": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, C.c_double, C.POINTER(C.c_double)]),

@@ -32,6 +32,67 @@ __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : 
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
 // ---------------------------------------------------------------------------
+// L2 eviction-priority hints.  Streams touched once per iteration (CSR
+// values/indices, state vectors) are loaded and stored evict_first so that the
+// randomly gathered vectors (x~ for G^ x~, y_hat for G^T y_hat) and the
+// freshly written y_hat / x~ keep their lines in the 126 MB L2.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_stream() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_keep() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// evict_last for a fraction of the lines (the rest evict_first): used when the
+// gathered vector is larger than the L2 set-aside, so a stable subset stays.
+__device__ __forceinline__ uint64_t policy_keep_frac(float f) {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(f));
+  return p;
+}
+// Measured on B200 (profiles/r01_*): with the hot SpMVs tiled so each
+// gathered slice fits in L2, plain LRU beats these policies, and a persisting
+// set-aside steals bandwidth from the streams -- so the hints compile to
+// plain loads/stores unless PDCS_L2_HINTS is defined.
+// The hints are a template switch of the step kernels (HINT) so both forms
+// can be measured; kL2Hints is the default of the plain helpers.
+constexpr bool kL2Hints = false;
+template <bool H = kL2Hints>
+__device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
+  if (!H) return __ldg(a);
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+template <bool H = kL2Hints>
+__device__ __forceinline__ int ld_hint(const int* a, uint64_t pol) {
+  if (!H) return __ldg(a);
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+// coherent (non-.nc) load for buffers the same kernel also writes
+template <bool H = kL2Hints>
+__device__ __forceinline__ double ldc_hint(const double* a, uint64_t pol) {
+  if (!H) return *a;
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+template <bool H = kL2Hints>
+__device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
+  if (!H) {
+    *a = v;
+    return;
+  }
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Deterministic reductions.  Sums go down a fixed shuffle tree to lane 0 and
 // are broadcast from there, so every lane sees the bit-identical value.
 // ---------------------------------------------------------------------------

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -69,6 +70,8 @@ KArgs make_args(const Engine* E) {
   A.ty0 = d.d_ty0; A.ty1 = d.d_ty1; A.ty2 = d.d_ty2;
   A.ctrl = E->d_ctrl;
   A.err = E->d_err;
+  A.keep_xt = E->keep_xt;
+  A.keep_yh = E->keep_yh;
   return A;
 }
 
@@ -83,7 +86,25 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
     CK(cudaStreamSynchronize(s));
   }
   P.vw = choose_vw(nnz, nrows);
-  P.long_t = std::max(256, 64 * P.vw);
+  P.long_t = TILE_NNZ;
+  // CSR-stream tiles over the short rows: <= TILE_ROWS rows, <= TILE_NNZ entries
+  std::vector<int> tiles(1, 0);
+  for (int r = 0; r < nrows;) {
+    int nz = 0, cnt = 0;
+    while (r < nrows && cnt < TILE_ROWS) {
+      int len = rp[r + 1] - rp[r];
+      if (len > P.long_t) len = 0;
+      if (cnt > 0 && nz + len > TILE_NNZ) break;
+      nz += len;
+      ++cnt;
+      ++r;
+    }
+    tiles.push_back(r);
+  }
+  P.ntiles = (int)tiles.size() - 1;
+  CK(cudaMalloc(&P.d_tiles, sizeof(int) * tiles.size()));
+  CK(cudaMemcpyAsync(P.d_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
   const int chunk = 2048;
   std::vector<int> lrows, lfirst;
   std::vector<int4> chunks;
@@ -117,6 +138,7 @@ void free_plan(SpmvPlan& P) {
   cudaFree(P.d_long_first);
   cudaFree(P.d_chunks);
   cudaFree(P.d_chunk_out);
+  cudaFree(P.d_tiles);
   P = SpmvPlan();
 }
 
@@ -218,19 +240,187 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
 }
 
 // ---- one line-search trial (graph slot) ----------------------------------
-template <int VW>
-int launch_step_y(Engine* E, const KArgs& A) {
-  k_step_y<VW><<<E->G.grid, BS, 0, E->stream>>>(A, E->G.nrows, E->G.rowptr, E->G.colidx, E->G.val,
-                                               E->G.long_t, E->d_partY, E->capY);
+// Final-pass source of a fused step SpMV: the last panel (after np-1 partial
+// passes into wpart) or the whole CSR.
+// Tile source of pass p of a panelled step SpMV (p = np-1: the fused last pass).
+TileSrc tile_source(const SpmvPlan& P, const PanelPlan& Q, int p, const double* wpart) {
+  TileSrc S;
+  S.tiles = P.d_tiles;
+  S.ntiles = P.ntiles;
+  S.po = Q.d_po + (size_t)p * P.nrows;
+  S.ci = Q.d_pci;
+  S.va = Q.d_pva;
+  S.wpart = p > 0 ? wpart : nullptr;
+  S.orig_rp = (p == Q.np - 1 && P.n_long) ? P.rowptr : nullptr;
+  S.long_t = P.long_t;
+  return S;
+}
+
+int launch_panel_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* x,
+                        double* wpart, int grid, int gate) {
+  for (int p = 0; p + 1 < Q.np; ++p) {
+    k_tile_pass<<<grid, BS, 0, E->stream>>>(tile_source(P, Q, p, wpart), x, wpart, E->d_ctrl, gate);
+    CKL();
+  }
+  return 0;
+}
+
+template <int VW, bool H>
+int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* x, double* wpart,
+                int gate, float keep) {
+  for (int p = 0; p + 1 < Q.np; ++p) {
+    k_lane_pass<VW, H><<<P.grid, BS, 0, E->stream>>>(tile_source(P, Q, p, wpart), P.nrows, x, wpart,
+                                                     E->d_ctrl, gate, keep);
+    CKL();
+  }
+  return 0;
+}
+
+template <int VW, bool H>
+int lane_y(Engine* E, const KArgs& A) {
+  if (lane_passes<VW, H>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
+  k_step_y_lane<VW, H><<<E->G.grid, BS, 0, E->stream>>>(
+      A, E->G.nrows, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY);
   CKL();
   return 0;
 }
-template <int VW>
-int launch_step_t(Engine* E, const KArgs& A) {
-  k_step_t<VW><<<E->GT.grid, BS, 0, E->stream>>>(A, E->GT.nrows, E->GT.rowptr, E->GT.colidx,
-                                                 E->GT.val, E->GT.long_t, E->d_partT, E->capT);
+
+template <int VW, bool H>
+int lane_t(Engine* E, const KArgs& A) {
+  if (lane_passes<VW, H>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
+  k_step_t_lane<VW, H><<<E->GT.grid, BS, 0, E->stream>>>(
+      A, E->GT.nrows, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT);
   CKL();
   return 0;
+}
+
+int launch_step_y(Engine* E, const KArgs& A) {
+  if (E->style_tile) {
+    if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
+    k_step_y<<<E->G.grid, BS, 0, E->stream>>>(A, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y),
+                                             E->d_partY, E->capY);
+    CKL();
+    return 0;
+  }
+  const bool h = E->hints;
+  switch (E->G.step_vw) {
+    case 1: return h ? lane_y<1, true>(E, A) : lane_y<1, false>(E, A);
+    case 8: return h ? lane_y<8, true>(E, A) : lane_y<8, false>(E, A);
+    default: return h ? lane_y<32, true>(E, A) : lane_y<32, false>(E, A);
+  }
+}
+
+int launch_step_t(Engine* E, const KArgs& A) {
+  if (E->style_tile) {
+    if (launch_panel_passes(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->GT.grid, 2)) return 1;
+    k_step_t<<<E->GT.grid, BS, 0, E->stream>>>(A, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x),
+                                               E->d_partT, E->capT);
+    CKL();
+    return 0;
+  }
+  const bool h = E->hints;
+  switch (E->GT.step_vw) {
+    case 1: return h ? lane_t<1, true>(E, A) : lane_t<1, false>(E, A);
+    case 8: return h ? lane_t<8, true>(E, A) : lane_t<8, false>(E, A);
+    default: return h ? lane_t<32, true>(E, A) : lane_t<32, false>(E, A);
+  }
+}
+
+// step-kernel lanes per row: 1 (short rows, index-order sums), 8 or 32
+int step_lanes(int64_t nnz, int64_t nrows) {
+  if (nrows <= 0) return 1;
+  const double mean = (double)nnz / (double)nrows;
+  return mean <= 6.0 ? 1 : (mean <= 24.0 ? 8 : 32);
+}
+
+const void* step_y_fn(const Engine* E) {
+  if (E->style_tile) return (const void*)k_step_y;
+  const bool h = E->hints;
+  switch (E->G.step_vw) {
+    case 1: return h ? (const void*)k_step_y_lane<1, true> : (const void*)k_step_y_lane<1, false>;
+    case 8: return h ? (const void*)k_step_y_lane<8, true> : (const void*)k_step_y_lane<8, false>;
+    default: return h ? (const void*)k_step_y_lane<32, true> : (const void*)k_step_y_lane<32, false>;
+  }
+}
+
+const void* step_t_fn(const Engine* E) {
+  if (E->style_tile) return (const void*)k_step_t;
+  const bool h = E->hints;
+  switch (E->GT.step_vw) {
+    case 1: return h ? (const void*)k_step_t_lane<1, true> : (const void*)k_step_t_lane<1, false>;
+    case 8: return h ? (const void*)k_step_t_lane<8, true> : (const void*)k_step_t_lane<8, false>;
+    default: return h ? (const void*)k_step_t_lane<32, true> : (const void*)k_step_t_lane<32, false>;
+  }
+}
+
+// Panelled copy of a CSR pattern (values filled by refresh_panel_values).
+int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
+  Q = PanelPlan();
+  Q.np = std::max(1, np);
+  if (P.nrows == 0) {
+    Q.np = 1;
+    return 0;
+  }
+  if (P.ncols < Q.np) Q.np = std::max(1, P.ncols);
+  Q.width = (P.ncols + Q.np - 1) / Q.np;
+  const size_t nflat = (size_t)Q.np * P.nrows;
+  int* cnt = nullptr;
+  CK(cudaMalloc(&cnt, sizeof(int) * (nflat + 1)));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (nflat + 1), s));
+  CK(cudaMalloc(&Q.d_po, sizeof(int) * (nflat + 1)));
+  k_panel_count<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width, cnt);
+  CKL();
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, Q.d_po, (int)(nflat + 1), s));
+  void* tmp = nullptr;
+  CK(cudaMalloc(&tmp, tmp_bytes));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, Q.d_po, (int)(nflat + 1), s));
+  int total = 0;
+  CK(cudaMemcpyAsync(&total, Q.d_po + nflat, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(tmp);
+  cudaFree(cnt);
+  Q.nnz_short = total;
+  CK(cudaMalloc(&Q.d_pci, sizeof(int) * std::max(total, 1)));
+  CK(cudaMalloc(&Q.d_pperm, sizeof(int) * std::max(total, 1)));
+  CK(cudaMalloc(&Q.d_pva, sizeof(double) * std::max(total, 1)));
+  k_panel_scatter<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width,
+                                                   Q.d_po, Q.d_pci, Q.d_pperm);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int refresh_panel_values(const PanelPlan& Q, const double* val, cudaStream_t s) {
+  if (Q.d_pva == nullptr || Q.nnz_short == 0) return 0;
+  k_gather<<<grid_for(Q.nnz_short), BS, 0, s>>>(Q.d_pva, val, Q.d_pperm, Q.nnz_short);
+  CKL();
+  return 0;
+}
+
+void free_panels(PanelPlan& Q) {
+  cudaFree(Q.d_po);
+  cudaFree(Q.d_pci);
+  cudaFree(Q.d_pva);
+  cudaFree(Q.d_pperm);
+  Q = PanelPlan();
+}
+
+// Optional per-stage event markers for pdcs_profile_slot (never active while
+// a graph is being captured).
+struct StageProf {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> names;
+} g_prof;
+
+void mark(cudaStream_t s, const char* name) {
+  if (!g_prof.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  g_prof.ev.push_back(e);
+  g_prof.names.push_back(name);
 }
 
 int launch_slot(Engine* E) {
@@ -238,41 +428,38 @@ int launch_slot(Engine* E) {
   cudaStream_t s = E->stream;
   BlkParams none{nullptr, nullptr, nullptr, 0, -1};
   // primal candidate
-  k_step_x<<<E->gridX, BS, 0, s>>>(A, E->d_partX, E->capX);
+  if (E->hints) k_step_x<true><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
+  else k_step_x<false><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
   CKL();
-  if (E->has_xblocks && launch_blocks<OP_STEP_X>(E->tabX, A, none, E->d_partX, E->capX, E->gridX, 1, s))
+  mark(s, "step_x");
+  if (E->has_xblocks && launch_blocks<OP_STEP_X>(E->tabX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s))
     return 1;
+  if (E->has_xblocks) mark(s, "blocks_x");
   // dual candidate with w = G^ x~
   if (E->G.n_long && launch_long(E->G, E->d.d_xt, E->d.d_w, E->d_ctrl, 1, s)) return 1;
+  if (E->G.n_long) mark(s, "long_rows_g");
   int rc = 0;
-  switch (E->G.vw) {
-    case 1: rc = launch_step_y<1>(E, A); break;
-    case 2: rc = launch_step_y<2>(E, A); break;
-    case 4: rc = launch_step_y<4>(E, A); break;
-    case 8: rc = launch_step_y<8>(E, A); break;
-    case 16: rc = launch_step_y<16>(E, A); break;
-    default: rc = launch_step_y<32>(E, A); break;
-  }
+  rc = launch_step_y(E, A);
   if (rc) return 1;
+  mark(s, "step_y_spmv");
   if (E->has_yblocks && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s))
     return 1;
+  if (E->has_yblocks) mark(s, "blocks_y");
   k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red);
   CKL();
+  mark(s, "ctrl_linesearch");
   // accepted: G^T y_hat, beta, Halpern coefficients
   if (E->GT.n_long && launch_long(E->GT, E->d.d_yh, E->d.d_gtr, E->d_ctrl, 2, s)) return 1;
-  switch (E->GT.vw) {
-    case 1: rc = launch_step_t<1>(E, A); break;
-    case 2: rc = launch_step_t<2>(E, A); break;
-    case 4: rc = launch_step_t<4>(E, A); break;
-    case 8: rc = launch_step_t<8>(E, A); break;
-    case 16: rc = launch_step_t<16>(E, A); break;
-    default: rc = launch_step_t<32>(E, A); break;
-  }
+  if (E->GT.n_long) mark(s, "long_rows_gt");
+  rc = launch_step_t(E, A);
   if (rc) return 1;
+  mark(s, "step_t_spmv");
   if (E->has_xblocks && launch_blocks<OP_TLAM>(E->tabX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s))
     return 1;
+  if (E->has_xblocks) mark(s, "blocks_t");
   k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err);
   CKL();
+  mark(s, "ctrl_beta");
   return 0;
 }
 
@@ -462,10 +649,71 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   if (build_plan(E->G, d.m, d.n, d.nnz, d.d_g_rowptr, d.d_g_colidx, d.d_g_val, s)) return fail(1);
   if (build_plan(E->GT, d.n, d.m, d.nnz, d.d_gt_rowptr, d.d_gt_colidx, d.d_gt_val, s)) return fail(1);
 
-  // grids and reduction capacities
+  // grids and reduction capacities: the streaming step kernels get exactly one
+  // wave of resident CTAs (grid-stride loops), the rest a capped grid
   E->gridX = grid_for(d.n);
   E->gridY = grid_for(d.m);
-  E->capX = E->gridX + E->tabX.grids();
+  {
+    int dev = 0, nsm = NSM, l2 = 126 << 20;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    // PDCS_TUNE="py=3,pt=2,panel_mb=48,gx=8,gy=5,gt=6" overrides (panels of the
+    // G^ / G^T step SpMVs, gathered-slice budget, CTAs per SM of step kernels)
+    auto tune = [](const char* key, double dflt) {
+      const char* env = getenv("PDCS_TUNE");
+      if (!env) return dflt;
+      std::string s(env), k = std::string(key) + "=";
+      size_t p = s.find(k);
+      if (p == std::string::npos || (p > 0 && s[p - 1] != ',')) return dflt;
+      return atof(s.c_str() + p + k.size());
+    };
+    // Column panels: cut the gathered vector into slices of at most 3/4 of L2
+    // (measured best on C5: 2 panels for G^ x~ (160 MB), 1 for G^T y_hat
+    // (80 MB); narrower panels pay more in partial sums than they save).
+    const double budget = tune("panel_mb", 0.75 * l2 / 1048576.0) * 1048576.0;
+    auto panels_for = [&](int ncols, int nrows, int nnz) {
+      if (nnz < (1 << 20)) return 1;  // small matrices: the whole vector is L2-resident
+      int np = (int)std::ceil(8.0 * ncols / budget);
+      return std::max(1, std::min(np, 16));
+    };
+    const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
+    const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
+    if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
+    E->style_tile = tune("tile", 0.0) > 0.0;
+    E->hints = tune("hints", 0.0) > 0.0;
+    E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
+    E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
+    if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
+      return fail(1);
+    if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)
+      return fail(1);
+    auto fit = [&](const void* fn, int needed) {
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BS, 0) != cudaSuccess || occ < 1) occ = 1;
+      return std::max(1, std::min(needed, occ * nsm));
+    };
+    auto grid_per_sm = [&](const char* key, int needed, int dflt) {
+      const int per = (int)tune(key, 0.0);
+      return per > 0 ? std::max(1, std::min(needed, per * nsm)) : dflt;
+    };
+    E->gridStepX = grid_per_sm("gx", E->gridX, E->gridX);
+    const int need_y = E->style_tile ? std::max(1, E->G.ntiles) : grid_for(d.m, BS / E->G.step_vw, 1 << 30);
+    const int need_t = E->style_tile ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
+    E->G.grid = grid_per_sm("gy", need_y, fit(step_y_fn(E), need_y));
+    E->GT.grid = grid_per_sm("gt", need_t, fit(step_t_fn(E), need_t));
+    // optional persisting-L2 set-aside (evict_last lines only persist inside it)
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    size_t want = E->hints ? (size_t)(tune("persist_mb", 0.0) * 1048576.0) : 0;
+    if (want > (size_t)max_persist) want = (size_t)max_persist;
+    if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+      E->l2_persist = want;
+    E->keep_xt = (float)tune("keep_xt", 1.0);
+    E->keep_yh = (float)tune("keep_yh", 1.0);
+    cudaGetLastError();
+  }
+  E->capX = E->gridStepX + E->tabX.grids();
   E->capY = E->G.grid + E->tabY.grids();
   E->capT = E->GT.grid + E->tabX.grids();
   E->capC = E->gridX + E->gridY + 2;
@@ -501,6 +749,10 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   if (E->graph) cudaGraphDestroy(E->graph);
   free_plan(E->G);
   free_plan(E->GT);
+  free_panels(E->PG);
+  free_panels(E->PGT);
+  cudaFree(E->d_wpart_y);
+  cudaFree(E->d_wpart_x);
   cudaFree(E->tabX.d_all);
   cudaFree(E->tabY.d_all);
   cudaFree(E->d_unif_x);
@@ -585,6 +837,8 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
     }
     k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
     CKL();
+    if (refresh_panel_values(E->PG, d.d_g_val, s) || refresh_panel_values(E->PGT, d.d_gt_val, s))
+      return 1;
   }
   k_scale_x<<<grid_for(n), BS, 0, s>>>(A, enabled == 2);
   CKL();
@@ -604,6 +858,16 @@ int pdcs_stats(PdcsEngine* E, double* h_out) {
   k_stats<<<g, BS, 0, s>>>(A, E->d.d_g_val, E->nnz, E->d.d_ty2, E->d_partC, E->capC);
   CKL();
   return finalize_to_host(E, E->d_partC, E->capC, g, 6, 0x30u, h_out);
+}
+
+int pdcs_engine_info(PdcsEngine* E, double* h_out) {
+  const double v[] = {(double)E->G.vw, (double)E->GT.vw, (double)E->gridStepX, (double)E->G.grid,
+                      (double)E->GT.grid, (double)E->keep_xt, (double)E->keep_yh,
+                      (double)E->l2_persist, (double)E->G.n_long, (double)E->GT.n_long,
+                      (double)E->tabX.total(), (double)E->tabY.total(), (double)E->PG.np,
+                      (double)E->PGT.np, (double)E->G.step_vw, (double)E->GT.step_vw};
+  std::memcpy(h_out, v, sizeof(v));
+  return 0;
 }
 
 int pdcs_engine_get_ctrl(PdcsEngine* E, PdcsCtrl* h) {
@@ -668,6 +932,38 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
     }
   }
   return 0;
+}
+
+int pdcs_profile_slot(PdcsEngine* E, int32_t reps, double* h_ms, const char** h_names, int32_t cap) {
+  cudaStream_t s = E->stream;
+  int count = 0;
+  std::vector<double> acc;
+  for (int r = 0; r < reps; ++r) {
+    g_prof.ev.clear();
+    g_prof.names.clear();
+    g_prof.on = true;
+    mark(s, "start");
+    int rc = launch_slot(E);
+    g_prof.on = false;
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s));
+    const int k = (int)g_prof.ev.size() - 1;
+    if (r == 0) {
+      count = k;
+      acc.assign(k, 0.0);
+    }
+    for (int i = 0; i < k && i < count; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, g_prof.ev[i], g_prof.ev[i + 1]));
+      acc[i] += ms;
+    }
+    for (auto e : g_prof.ev) cudaEventDestroy(e);
+  }
+  for (int i = 0; i < count && i < cap; ++i) {
+    h_ms[i] = acc[i] / reps;
+    h_names[i] = g_prof.names[i + 1];
+  }
+  return count;
 }
 
 int pdcs_flush(PdcsEngine* E) {

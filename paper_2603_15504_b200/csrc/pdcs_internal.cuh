@@ -20,6 +20,7 @@ struct SpmvPlan {
   const int* colidx = nullptr;
   const double* val = nullptr;
   int vw = 1;
+  int step_vw = 1;  // lanes per row of the fused step kernels (panel rows are shorter)
   int long_t = 1 << 30;
   int n_long = 0, n_chunks = 0;
   int* d_long_rows = nullptr;     // [n_long]
@@ -27,6 +28,25 @@ struct SpmvPlan {
   int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
   double* d_chunk_out = nullptr;  // [n_chunks]
   int grid = 1;                   // CTAs of the short-row kernel
+  int* d_tiles = nullptr;         // [ntiles + 1] CSR-stream tile boundaries (rows)
+  int ntiles = 0;
+};
+
+// Column-panelled copy of a CSR matrix for the fused step SpMVs: columns are
+// cut into `np` equal ranges so the slice of the gathered vector a pass reads
+// fits in L2; pass p sums row i's entries of panel p on top of the partial
+// of passes 0..p-1 (index order is preserved, so a thread-per-row sum is
+// still bit-identical to scipy's csr_matvec).  Long rows are left out (they
+// go through the chunked path).  Offsets are flattened [panel][row]: panel
+// p's row i spans po[p*nrows + i] .. po[p*nrows + i + 1].
+struct PanelPlan {
+  int np = 1;
+  int width = 0;
+  int* d_po = nullptr;      // [np*nrows + 1]
+  int* d_pci = nullptr;     // [nnz_short] absolute column indices
+  double* d_pva = nullptr;  // [nnz_short]
+  int* d_pperm = nullptr;   // [nnz_short] position in the CSR
+  int nnz_short = 0;
 };
 
 // Cone-block table of one space split into size classes.
@@ -38,6 +58,8 @@ struct BlockTable {
   int grids() const { return g_thread + g_warp + g_cta; }
 };
 
+constexpr int TILE_ROWS = BS;    // rows per CSR-stream tile (one per thread in phase 2)
+constexpr int TILE_NNZ = 2048;   // entries per tile; longer rows use the chunked path
 constexpr int WARP_CLASS_MAX = 4096;  // dims above this get a whole CTA
 constexpr int THREAD_CLASS_MAX = 4;   // dims up to this get one thread
 constexpr int CTA_BLOCK_THREADS = 512;
@@ -55,6 +77,9 @@ struct Engine {
   int allow_nonuniform_dual_soc = 0;
 
   SpmvPlan G, GT;  // G^ (m x n) and G^T (n x m)
+  PanelPlan PG, PGT;  // panelled copies used by the fused step kernels
+  double* d_wpart_y = nullptr;  // partial sums of the G^ passes  [m]
+  double* d_wpart_x = nullptr;  // partial sums of the G^T passes [n]
   BlockTable tabX, tabY;
   bool has_xblocks = false, has_yblocks = false;
   // uniformity groups for preconditioning (blocks whose scale is made uniform)
@@ -71,6 +96,11 @@ struct Engine {
   double* d_partT = nullptr;
   int capX = 0, capY = 0, capT = 0;
   int gridX = 1, gridXE = 1;  // x-space streaming grid
+  int gridStepX = 1;          // k_step_x grid (one wave of resident CTAs)
+  float keep_xt = 1.0f, keep_yh = 1.0f;  // evict_last fractions (L2 set-aside / vector bytes)
+  bool style_tile = false;  // step SpMVs: tiled CSR-stream (true) or lane-mapped (false)
+  bool hints = false;       // L2 eviction-priority hints in the step kernels
+  size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)
   double* d_partC = nullptr;  // check path partials [PDCS_NMET*2][capC]
   int capC = 0;

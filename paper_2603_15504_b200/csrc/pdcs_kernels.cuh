@@ -13,6 +13,7 @@ struct KArgs {
   double *tx0, *tx1, *tx2, *ty0, *ty1, *ty2;
   PdcsCtrl* ctrl;
   int* err;
+  float keep_xt, keep_yh;  // evict_last fractions of the gathered x~ / y_hat lines
 };
 
 // gate: 0 = always run, 1 = skip when stopped, 2 = skip when stopped or the
@@ -97,19 +98,64 @@ __device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int*
                                           const double* __restrict__ va,
                                           const double* __restrict__ x, int row, int sub,
                                           int nrows, int long_t, const double* longv,
-                                          bool& lng) {
+                                          bool& lng, uint64_t pk) {
   double s = 0.0;
   lng = false;
   if (row < nrows) {
-    const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+    const uint64_t ps = policy_stream();
+    const int b = ld_hint(rp + row, ps), e = ld_hint(rp + row + 1, ps);
     if (e - b > long_t) {
       lng = true;
       if (sub == 0) s = longv[row];
+    } else if (VW == 1) {
+      // thread per row: issue four index loads, then four gathers, then
+      // accumulate in index order (the sum order of scipy's csr_matvec)
+      int j = b;
+      for (; j + 4 <= e; j += 4) {
+        const int c0 = ld_hint(ci + j, ps), c1 = ld_hint(ci + j + 1, ps);
+        const int c2 = ld_hint(ci + j + 2, ps), c3 = ld_hint(ci + j + 3, ps);
+        const double a0 = ld_hint(va + j, ps), a1 = ld_hint(va + j + 1, ps);
+        const double a2 = ld_hint(va + j + 2, ps), a3 = ld_hint(va + j + 3, ps);
+        const double x0 = ld_hint(x + c0, pk), x1 = ld_hint(x + c1, pk);
+        const double x2 = ld_hint(x + c2, pk), x3 = ld_hint(x + c3, pk);
+        s += a0 * x0;
+        s += a1 * x1;
+        s += a2 * x2;
+        s += a3 * x3;
+      }
+      for (; j < e; ++j) s += ld_hint(va + j, ps) * ld_hint(x + ld_hint(ci + j, ps), pk);
     } else {
-      for (int j = b + sub; j < e; j += VW) s += __ldg(va + j) * __ldg(x + __ldg(ci + j));
+      for (int j = b + sub; j < e; j += VW) s += ld_hint(va + j, ps) * ld_hint(x + ld_hint(ci + j, ps), pk);
     }
   }
   if (VW > 1) {
+#pragma unroll
+    for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
+  }
+  return s;
+}
+
+// Dot product of one row segment [b, e) with the gathered vector x, started
+// from s0 (lane 0 of the VW group carries it).  VW = 1 sums in index order.
+template <int VW>
+__device__ __forceinline__ double seg_dot(const int* __restrict__ ci, const double* __restrict__ va,
+                                          const double* __restrict__ x, int b, int e, int sub,
+                                          double s0) {
+  double s = sub == 0 ? s0 : 0.0;
+  if (VW == 1) {
+    int j = b;
+    for (; j + 4 <= e; j += 4) {
+      const int c0 = __ldg(ci + j), c1 = __ldg(ci + j + 1), c2 = __ldg(ci + j + 2), c3 = __ldg(ci + j + 3);
+      const double a0 = __ldg(va + j), a1 = __ldg(va + j + 1), a2 = __ldg(va + j + 2), a3 = __ldg(va + j + 3);
+      const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+      s += a0 * x0;
+      s += a1 * x1;
+      s += a2 * x2;
+      s += a3 * x3;
+    }
+    for (; j < e; ++j) s += __ldg(va + j) * __ldg(x + __ldg(ci + j));
+  } else {
+    for (int j = b + sub; j < e; j += VW) s += __ldg(va + j) * __ldg(x + __ldg(ci + j));
 #pragma unroll
     for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
   }
@@ -131,7 +177,7 @@ __global__ void __launch_bounds__(BS) k_spmv(int nrows, const int* __restrict__ 
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int row = base + lane / VW;
     bool lng;
-    double s = row_dot<VW>(rp, ci, va, x, row, sub, nrows, long_t, y, lng);
+    double s = row_dot<VW>(rp, ci, va, x, row, sub, nrows, long_t, y, lng, policy_stream());
     if (sub == 0 && row < nrows && !lng) y[row] = s;
   }
 }
@@ -160,6 +206,42 @@ __global__ void k_long_final(const int* __restrict__ rows, const int* __restrict
   double s = 0.0;
   for (int c = first[i]; c < first[i + 1]; ++c) s += part[c];
   y[rows[i]] = s;
+}
+
+// Panel build: entries per (panel, row); long rows get none.
+__global__ void k_panel_count(int nrows, const int* __restrict__ rp, const int* __restrict__ ci,
+                              int long_t, int np, int width, int* cnt) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int b = rp[r], e = rp[r + 1];
+    const bool lng = e - b > long_t;
+    int j = b;
+    for (int p = 0; p < np; ++p) {
+      const long long lim = (long long)(p + 1) * width;
+      int c = 0;
+      while (!lng && j < e && ci[j] < lim) { ++c; ++j; }
+      cnt[(long long)p * nrows + r] = c;
+    }
+  }
+}
+// Panel build: scatter column indices and CSR positions in panel-major order.
+__global__ void k_panel_scatter(int nrows, const int* __restrict__ rp, const int* __restrict__ ci,
+                                int long_t, int np, int width, const int* __restrict__ po, int* pci,
+                                int* pperm) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const int b = rp[r], e = rp[r + 1];
+    if (e - b > long_t) continue;
+    int j = b;
+    for (int p = 0; p < np; ++p) {
+      const long long lim = (long long)(p + 1) * width;
+      int pos = po[(long long)p * nrows + r];
+      while (j < e && ci[j] < lim) {
+        pci[pos] = ci[j];
+        pperm[pos] = j;
+        ++pos;
+        ++j;
+      }
+    }
+  }
 }
 
 // Row reductions used by the preconditioner: OP 0 = max |a_ij| (order free),
@@ -435,7 +517,8 @@ __global__ void __launch_bounds__(CTA_BLOCK_THREADS) k_blk_cta(const PdcsBlock* 
 // candidate x_hat = P_X(x - tau (c - G^T y)), x~ = 2 x_hat - x and the
 // reductions ||x||^2, ||x_hat - x||^2, c.x_hat (engine.py:155-161, 207-218,
 // 246-277, 602-610).  Cone coordinates are left unprojected for k_blk_*.
-__global__ void __launch_bounds__(BS) k_step_x(KArgs A, double* part, int cap) {
+template <bool H>
+__global__ void __launch_bounds__(BS, 5) k_step_x(KArgs A, double* part, int cap) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   const bool pend = C->pending != 0;
@@ -443,27 +526,28 @@ __global__ void __launch_bounds__(BS) k_step_x(KArgs A, double* part, int cap) {
   const double opb = 1.0 + be, tot = W + et;
   const bool inject = C->nan_after >= 0 && C->n_primal_proj >= C->nan_after;
   double acc[GX_N] = {0.0, 0.0, 0.0};
+  const uint64_t ps = policy_stream(), pk = policy_keep_frac(A.keep_xt);
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x) {
     double xn, gn;
     if (pend) {
-      const double xo = A.x[j];
-      xn = a * (opb * A.xh[j] - be * xo) + b * A.xa[j];
-      const double go = A.gty[j];
-      gn = a * (opb * A.gth[j] - be * go) + b * A.gtya[j];
-      A.xb[j] = (W == 0.0) ? xn : (W * A.xb[j] + et * xn) / tot;
-      A.x[j] = xn;
-      A.gty[j] = gn;
+      const double xo = ldc_hint<H>(A.x + j, ps);
+      xn = a * (opb * ldc_hint<H>(A.xh + j, ps) - be * xo) + b * ld_hint<H>(A.xa + j, ps);
+      const double go = ldc_hint<H>(A.gty + j, ps);
+      gn = a * (opb * ld_hint<H>(A.gth + j, ps) - be * go) + b * ld_hint<H>(A.gtya + j, ps);
+      st_hint<H>(A.xb + j, (W == 0.0) ? xn : (W * ldc_hint<H>(A.xb + j, ps) + et * xn) / tot, ps);
+      st_hint<H>(A.x + j, xn, ps);
+      st_hint<H>(A.gty + j, gn, ps);
     } else {
-      xn = A.x[j];
-      gn = A.gty[j];
+      xn = ldc_hint<H>(A.x + j, ps);
+      gn = ldc_hint<H>(A.gty + j, ps);
     }
-    const double cj = A.c[j];
+    const double cj = ld_hint<H>(A.c + j, ps);
     const double v = xn - tau * (cj - gn);
     if (j < A.nbox) {
-      double p = clampv(v, A.l[j], A.u[j]);
+      double p = clampv(v, ld_hint<H>(A.l + j, ps), ld_hint<H>(A.u + j, ps));
       if (j == 0 && inject) p = __longlong_as_double(0x7ff8000000000000ll);
-      A.xh[j] = p;
-      A.xt[j] = 2.0 * p - xn;
+      st_hint<H>(A.xh + j, p, ps);
+      st_hint<H>(A.xt + j, 2.0 * p - xn, pk);
       const double d = p - xn;
       acc[GX_XX] += xn * xn;
       acc[GX_DXDX] += d * d;
@@ -475,20 +559,248 @@ __global__ void __launch_bounds__(BS) k_step_x(KArgs A, double* part, int cap) {
   block_store_mask<GX_N>(acc, 0u, part, cap, blockIdx.x);
 }
 
-// y-space fused with w = G^ x~: pending Halpern/average, then
+// ---- tiled CSR-stream SpMV ---------------------------------------------------
+// A tile is up to TILE_ROWS consecutive rows holding at most TILE_NNZ entries
+// (of the current panel).  Phase 1 streams the tile's (col, val) coalesced and
+// issues all of its gathers at once, parking the products in shared memory;
+// phase 2 gives each row to one thread, which adds its products in index
+// order -- the exact rounding sequence of scipy's csr_matvec (s += a*x).
+struct TileSrc {
+  const int* tiles;     // [ntiles + 1] first row of each tile
+  int ntiles;
+  const int* po;        // row offsets of this pass (panel) into ci/va
+  const int* ci;
+  const double* va;
+  const double* wpart;  // partial sums of the previous passes (nullptr: start at 0)
+  const int* orig_rp;   // rows longer than long_t in the CSR take longv (nullptr: none)
+  int long_t;
+};
+
+__device__ __forceinline__ double tile_rows(const TileSrc& S, const double* __restrict__ x,
+                                            const double* longv, int r0, int nr, double* prod,
+                                            int* rs) {
+  const int base = __ldg(S.po + r0);
+  const int tnnz = __ldg(S.po + r0 + nr) - base;
+  for (int i = threadIdx.x; i <= nr; i += blockDim.x) rs[i] = __ldg(S.po + r0 + i) - base;
+  const int* __restrict__ ci = S.ci + base;
+  const double* __restrict__ va = S.va + base;
+  int k = threadIdx.x;
+  for (; k + 3 * BS < tnnz; k += 4 * BS) {
+    const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + BS), c2 = __ldg(ci + k + 2 * BS),
+              c3 = __ldg(ci + k + 3 * BS);
+    const double a0 = __ldg(va + k), a1 = __ldg(va + k + BS), a2 = __ldg(va + k + 2 * BS),
+                 a3 = __ldg(va + k + 3 * BS);
+    const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
+    prod[k] = a0 * x0;
+    prod[k + BS] = a1 * x1;
+    prod[k + 2 * BS] = a2 * x2;
+    prod[k + 3 * BS] = a3 * x3;
+  }
+  for (; k < tnnz; k += BS) prod[k] = __ldg(va + k) * __ldg(x + __ldg(ci + k));
+  __syncthreads();
+  double s = 0.0;
+  const int i = threadIdx.x;
+  if (i < nr) {
+    const int r = r0 + i;
+    const bool lng = S.orig_rp && (__ldg(S.orig_rp + r + 1) - __ldg(S.orig_rp + r)) > S.long_t;
+    if (lng) {
+      s = longv[r];
+    } else {
+      if (S.wpart) s = S.wpart[r];
+      for (int q = rs[i]; q < rs[i + 1]; ++q) s += prod[q];
+    }
+  }
+  return s;
+}
+
+// One partial pass of a panelled SpMV (all panels but the last).
+__global__ void __launch_bounds__(BS) k_tile_pass(TileSrc S, const double* __restrict__ x,
+                                                  double* wout, const PdcsCtrl* ctrl, int gate) {
+  if (gated(ctrl, gate)) return;
+  __shared__ double prod[TILE_NNZ];
+  __shared__ int rs[TILE_ROWS + 1];
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+    const int r0 = __ldg(S.tiles + t), nr = __ldg(S.tiles + t + 1) - r0;
+    const double s = tile_rows(S, x, nullptr, r0, nr, prod, rs);
+    if (threadIdx.x < nr) wout[r0 + threadIdx.x] = s;
+    __syncthreads();
+  }
+}
+
+// ---- per-row epilogues of the fused step kernels -----------------------------
+struct YCoef {
+  bool pend;
+  double a, b, be, et, W, sigma, opb, tot;
+};
+
+__device__ __forceinline__ YCoef y_coef(const PdcsCtrl* C) {
+  YCoef k;
+  k.pend = C->pending != 0;
+  k.a = C->pa; k.b = C->pb; k.be = C->pbeta; k.et = C->peta; k.W = C->pW; k.sigma = C->sigma;
+  k.opb = 1.0 + k.be;
+  k.tot = k.W + k.et;
+  return k;
+}
+
+// y-space row r with dot = (G^ x~)_r: pending Halpern/average, then
 // y_hat = P_Y(y + sigma (h - w)), gx_hat = (w + gx)/2 and the reductions
 // ||y||^2, ||dy||^2, dy.(w - gx), the beta residual ||r - P_{K_d*} r||^2 of
 // r = gx_hat - h, and y_hat.h.  Block rows are left for k_blk_*.
-template <int VW>
-__global__ void __launch_bounds__(BS) k_step_y(KArgs A, int nrows, const int* __restrict__ rp,
-                                               const int* __restrict__ ci,
-                                               const double* __restrict__ va, int long_t,
-                                               double* part, int cap) {
+template <bool H>
+__device__ __forceinline__ void y_epilogue(const KArgs& A, const YCoef& k, int r, double dot,
+                                           double* acc, uint64_t ps, uint64_t pk) {
+  double yn, gn;
+  if (k.pend) {
+    const double yo = ldc_hint<H>(A.y + r, ps);
+    yn = k.a * (k.opb * ldc_hint<H>(A.yh + r, ps) - k.be * yo) + k.b * ld_hint<H>(A.ya + r, ps);
+    const double go = ldc_hint<H>(A.gx + r, ps);
+    gn = k.a * (k.opb * ldc_hint<H>(A.gxh + r, ps) - k.be * go) + k.b * ld_hint<H>(A.gxa + r, ps);
+    st_hint<H>(A.yb + r, (k.W == 0.0) ? yn : (k.W * ldc_hint<H>(A.yb + r, ps) + k.et * yn) / k.tot, ps);
+    st_hint<H>(A.y + r, yn, ps);
+    st_hint<H>(A.gx + r, gn, ps);
+  } else {
+    yn = ldc_hint<H>(A.y + r, ps);
+    gn = ldc_hint<H>(A.gx + r, ps);
+  }
+  const double hi = ld_hint<H>(A.h + r, ps);
+  const double v = yn + k.sigma * (hi - dot);
+  const double gh = 0.5 * (dot + gn);
+  st_hint<H>(A.gxh + r, gh, ps);
+  if (r < A.m_elem) {
+    const bool zero = r < A.m_zero;
+    const double p = zero ? v : pos_part(v);
+    st_hint<H>(A.yh + r, p, pk);
+    const double dy = p - yn;
+    acc[GY_YY] += yn * yn;
+    acc[GY_DYDY] += dy * dy;
+    acc[GY_INTER] += dy * (dot - gn);
+    const double res = gh - hi;
+    const double viol = zero ? res : res - pos_part(res);
+    acc[GY_RP2] += viol * viol;
+    acc[GY_YH] += p * hi;
+  } else {
+    A.yh[r] = v;
+    A.w[r] = dot;
+  }
+}
+
+// x-space row j with dot = (G^T y_hat)_j: stores gth and the box part of the
+// dual residual of beta, ||lam1 - P_Lambda lam1||^2, and the bound terms of
+// the dual objective (model.py:182-237, termination.py:113-119).
+template <bool H>
+__device__ __forceinline__ void t_epilogue(const KArgs& A, int j, double dot, double* acc,
+                                           uint64_t ps) {
+  st_hint<H>(A.gth + j, dot, ps);
+  if (j < A.nbox) {
+    const double lam = ld_hint<H>(A.c + j, ps) - dot;
+    const double lj = ld_hint<H>(A.l + j, ps), uj = ld_hint<H>(A.u + j, ps);
+    const bool lf = isfinite(lj), uf = isfinite(uj);
+    const double pr = (!lf && !uf) ? 0.0 : (!lf ? neg_clip(lam) : (!uf ? pos_part(lam) : lam));
+    const double v = lam - pr;
+    acc[GT_RD2] += v * v;
+    if (lf) acc[GT_LSUM] += lj * pos_part(lam);
+    if (uf) acc[GT_USUM] += uj * pos_part(-lam);
+  }
+}
+
+// ---- tiled (CSR-stream) step kernels -----------------------------------------
+__global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* part, int cap) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
-  const bool pend = C->pending != 0;
-  const double a = C->pa, b = C->pb, be = C->pbeta, et = C->peta, W = C->pW, sigma = C->sigma;
-  const double opb = 1.0 + be, tot = W + et;
+  __shared__ double prod[TILE_NNZ];
+  __shared__ int rs[TILE_ROWS + 1];
+  const YCoef k = y_coef(C);
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+    const int r0 = __ldg(S.tiles + t), nr = __ldg(S.tiles + t + 1) - r0;
+    const double dot = tile_rows(S, A.xt, A.w, r0, nr, prod, rs);
+    if (threadIdx.x < nr) y_epilogue<false>(A, k, r0 + threadIdx.x, dot, acc, 0, 0);
+    __syncthreads();
+  }
+  block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* part, int cap) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop || !C->accepted) return;
+  __shared__ double prod[TILE_NNZ];
+  __shared__ int rs[TILE_ROWS + 1];
+  double acc[GT_N] = {0.0, 0.0, 0.0};
+  for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
+    const int r0 = __ldg(S.tiles + t), nr = __ldg(S.tiles + t + 1) - r0;
+    const double dot = tile_rows(S, A.yh, A.gtr, r0, nr, prod, rs);
+    if (threadIdx.x < nr) t_epilogue<false>(A, r0 + threadIdx.x, dot, acc, 0);
+    __syncthreads();
+  }
+  block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+}
+
+// ---- lane-mapped step kernels: VW lanes per row ------------------------------
+template <int VW, bool H>
+__device__ __forceinline__ double lane_row(const TileSrc& S, const double* __restrict__ x,
+                                           const double* longv, int r, int sub, int nrows,
+                                           uint64_t ps, uint64_t pk) {
+  int b = 0, e = 0;
+  double s = 0.0;
+  if (r < nrows) {
+    const bool lng = S.orig_rp && (__ldg(S.orig_rp + r + 1) - __ldg(S.orig_rp + r)) > S.long_t;
+    if (lng) {
+      if (sub == 0) s = longv[r];
+    } else {
+      b = ld_hint<H>(S.po + r, ps);
+      e = ld_hint<H>(S.po + r + 1, ps);
+      if (S.wpart && sub == 0) s = S.wpart[r];
+    }
+  }
+  if (VW == 1) {
+    int j = b;
+    for (; j + 4 <= e; j += 4) {
+      const int c0 = ld_hint<H>(S.ci + j, ps), c1 = ld_hint<H>(S.ci + j + 1, ps);
+      const int c2 = ld_hint<H>(S.ci + j + 2, ps), c3 = ld_hint<H>(S.ci + j + 3, ps);
+      const double a0 = ld_hint<H>(S.va + j, ps), a1 = ld_hint<H>(S.va + j + 1, ps);
+      const double a2 = ld_hint<H>(S.va + j + 2, ps), a3 = ld_hint<H>(S.va + j + 3, ps);
+      const double x0 = ld_hint<H>(x + c0, pk), x1 = ld_hint<H>(x + c1, pk);
+      const double x2 = ld_hint<H>(x + c2, pk), x3 = ld_hint<H>(x + c3, pk);
+      s += a0 * x0;
+      s += a1 * x1;
+      s += a2 * x2;
+      s += a3 * x3;
+    }
+    for (; j < e; ++j) s += ld_hint<H>(S.va + j, ps) * ld_hint<H>(x + ld_hint<H>(S.ci + j, ps), pk);
+  } else {
+    for (int j = b + sub; j < e; j += VW)
+      s += ld_hint<H>(S.va + j, ps) * ld_hint<H>(x + ld_hint<H>(S.ci + j, ps), pk);
+#pragma unroll
+    for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
+  }
+  return s;
+}
+
+template <int VW, bool H>
+__global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const double* __restrict__ x,
+                                                  double* wout, const PdcsCtrl* ctrl, int gate,
+                                                  float keep) {
+  if (gated(ctrl, gate)) return;
+  const uint64_t ps = policy_stream(), pk = policy_keep_frac(keep);
+  const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
+  constexpr int RPW = 32 / VW;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wt = gridDim.x * (blockDim.x >> 5);
+  for (int base = wg * RPW; base < nrows; base += wt * RPW) {
+    const int r = base + lane / VW;
+    const double s = lane_row<VW, H>(S, x, nullptr, r, sub, nrows, ps, pk);
+    if (sub == 0 && r < nrows) wout[r] = s;
+  }
+}
+
+template <int VW, bool H>
+__global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
+                                                       int cap) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  const YCoef k = y_coef(C);
+  const uint64_t ps = policy_stream(), pkx = policy_keep_frac(A.keep_xt),
+                 pky = policy_keep_frac(A.keep_yh);
   double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
   constexpr int RPW = 32 / VW;
@@ -496,57 +808,18 @@ __global__ void __launch_bounds__(BS) k_step_y(KArgs A, int nrows, const int* __
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int r = base + lane / VW;
-    bool lng;
-    const double dot = row_dot<VW>(rp, ci, va, A.xt, r, sub, nrows, long_t, A.w, lng);
-    if (sub == 0 && r < nrows) {
-      double yn, gn;
-      if (pend) {
-        const double yo = A.y[r];
-        yn = a * (opb * A.yh[r] - be * yo) + b * A.ya[r];
-        const double go = A.gx[r];
-        gn = a * (opb * A.gxh[r] - be * go) + b * A.gxa[r];
-        A.yb[r] = (W == 0.0) ? yn : (W * A.yb[r] + et * yn) / tot;
-        A.y[r] = yn;
-        A.gx[r] = gn;
-      } else {
-        yn = A.y[r];
-        gn = A.gx[r];
-      }
-      const double hi = A.h[r];
-      const double v = yn + sigma * (hi - dot);
-      const double gh = 0.5 * (dot + gn);
-      A.gxh[r] = gh;
-      if (r < A.m_elem) {
-        const bool zero = r < A.m_zero;
-        const double p = zero ? v : pos_part(v);
-        A.yh[r] = p;
-        const double dy = p - yn;
-        acc[GY_YY] += yn * yn;
-        acc[GY_DYDY] += dy * dy;
-        acc[GY_INTER] += dy * (dot - gn);
-        const double res = gh - hi;
-        const double viol = zero ? res : res - pos_part(res);
-        acc[GY_RP2] += viol * viol;
-        acc[GY_YH] += p * hi;
-      } else {
-        A.yh[r] = v;
-        A.w[r] = dot;
-      }
-    }
+    const double dot = lane_row<VW, H>(S, A.xt, A.w, r, sub, nrows, ps, pkx);
+    if (sub == 0 && r < nrows) y_epilogue<H>(A, k, r, dot, acc, ps, pky);
   }
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
 }
 
-// x-space fused with gth = G^T y_hat (accepted trials only): stores gth and the
-// box part of the dual residual of beta: ||lam1 - P_Lambda lam1||^2 and the
-// bound terms of the dual objective (model.py:182-237, termination.py:113-119).
-template <int VW>
-__global__ void __launch_bounds__(BS) k_step_t(KArgs A, int nrows, const int* __restrict__ rp,
-                                               const int* __restrict__ ci,
-                                               const double* __restrict__ va, int long_t,
-                                               double* part, int cap) {
+template <int VW, bool H>
+__global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
+                                                       int cap) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
+  const uint64_t ps = policy_stream(), pky = policy_keep_frac(A.keep_yh);
   double acc[GT_N] = {0.0, 0.0, 0.0};
   const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
   constexpr int RPW = 32 / VW;
@@ -554,21 +827,8 @@ __global__ void __launch_bounds__(BS) k_step_t(KArgs A, int nrows, const int* __
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int j = base + lane / VW;
-    bool lng;
-    const double dot = row_dot<VW>(rp, ci, va, A.yh, j, sub, nrows, long_t, A.gtr, lng);
-    if (sub == 0 && j < nrows) {
-      A.gth[j] = dot;
-      if (j < A.nbox) {
-        const double lam = A.c[j] - dot;
-        const double lj = A.l[j], uj = A.u[j];
-        const bool lf = isfinite(lj), uf = isfinite(uj);
-        const double pr = (!lf && !uf) ? 0.0 : (!lf ? neg_clip(lam) : (!uf ? pos_part(lam) : lam));
-        const double v = lam - pr;
-        acc[GT_RD2] += v * v;
-        if (lf) acc[GT_LSUM] += lj * pos_part(lam);
-        if (uf) acc[GT_USUM] += uj * pos_part(-lam);
-      }
-    }
+    const double dot = lane_row<VW, H>(S, A.yh, A.gtr, j, sub, nrows, ps, pky);
+    if (sub == 0 && j < nrows) t_epilogue<H>(A, j, dot, acc, ps);
   }
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
 }

@@ -223,6 +223,14 @@ class DeviceEngine:
         N.check(self.lib.pdcs_stats(self.handle, out), "pdcs_stats")
         return dict(c1=out[0], h1=out[1], c2=out[2], h2=out[3], gmax=out[4], rowsum_max=out[5])
 
+    def info(self) -> dict:
+        out = (C.c_double * 16)()
+        N.check(self.lib.pdcs_engine_info(self.handle, out), "pdcs_engine_info")
+        keys = ["vw_g", "vw_gt", "grid_step_x", "grid_step_y", "grid_step_t", "keep_xt", "keep_yh",
+                "l2_persist_bytes", "long_rows_g", "long_rows_gt", "primal_blocks", "dual_blocks",
+                "panels_g", "panels_gt", "step_vw_g", "step_vw_gt"]
+        return {k: out[i] for i, k in enumerate(keys)}
+
     def get_ctrl(self) -> N.PdcsCtrl:
         c = N.PdcsCtrl()
         N.check(self.lib.pdcs_engine_get_ctrl(self.handle, C.byref(c)), "pdcs_engine_get_ctrl")
@@ -233,6 +241,17 @@ class DeviceEngine:
 
     def run_inner(self, slots: int):
         N.check(self.lib.pdcs_run_inner(self.handle, int(slots)), "pdcs_run_inner")
+
+    def profile_slot(self, reps: int):
+        """Per-stage device times (ms) of `reps` eager line-search trials."""
+        ms = (C.c_double * 32)()
+        names = (C.c_char_p * 32)()
+        k = self.lib.pdcs_profile_slot(self.handle, int(reps), ms, names, 32)
+        if k < 0 or k > 32:
+            N.check(1, "pdcs_profile_slot")
+        if k == 1 and names[0] is None:
+            N.check(1, "pdcs_profile_slot")
+        return [(names[i].decode(), ms[i]) for i in range(k)]
 
     def flush(self):
         N.check(self.lib.pdcs_flush(self.handle), "pdcs_flush")

@@ -105,7 +105,7 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   CK(cudaMalloc(&P.d_tiles, sizeof(int) * tiles.size()));
   CK(cudaMemcpyAsync(P.d_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
-  const int chunk = 2048;
+  const int chunk = 8192;
   std::vector<int> lrows, lfirst;
   std::vector<int4> chunks;
   for (int r = 0; r < nrows; ++r) {
@@ -192,29 +192,44 @@ int launch_rowred(const SpmvPlan& P, const double* val, double* out, cudaStream_
 }
 
 // ---- cone block tables -------------------------------------------------------
-int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s) {
-  std::vector<PdcsBlock> th, wa, ct;
+int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bool giant_ok = false) {
+  std::vector<PdcsBlock> th, wa, ct, gi;
   for (auto& b : blocks) {
     if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
     else if (b.dim <= WARP_CLASS_MAX) wa.push_back(b);
+    else if (giant_ok && b.kind == PDCS_SOC && b.dim > GIANT_MIN) gi.push_back(b);
     else ct.push_back(b);
   }
   T.n_thread = (int)th.size();
   T.n_warp = (int)wa.size();
   T.n_cta = (int)ct.size();
+  T.n_giant = (int)gi.size();
   std::vector<PdcsBlock> all;
   all.insert(all.end(), th.begin(), th.end());
   all.insert(all.end(), wa.begin(), wa.end());
   all.insert(all.end(), ct.begin(), ct.end());
+  all.insert(all.end(), gi.begin(), gi.end());
   T.g_thread = T.n_thread ? grid_for(T.n_thread) : 0;
   T.g_warp = T.n_warp ? grid_for(T.n_warp, BS / 32) : 0;
   T.g_cta = T.n_cta ? std::min(T.n_cta, MAX_GRID) : 0;
+  T.g_giant = T.n_giant ? GIANT_GRID : 0;
   if (!all.empty()) {
     CK(cudaMalloc(&T.d_all, sizeof(PdcsBlock) * all.size()));
     CK(cudaMemcpyAsync(T.d_all, all.data(), sizeof(PdcsBlock) * all.size(), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
   }
+  if (T.n_giant) {
+    CK(cudaMalloc(&T.d_gpart, sizeof(double) * 2 * T.g_giant * T.n_giant));
+    CK(cudaMalloc(&T.d_gcoef, sizeof(double) * 8 * T.n_giant));
+  }
   return 0;
+}
+
+void free_table(BlockTable& T) {
+  cudaFree(T.d_all);
+  cudaFree(T.d_gpart);
+  cudaFree(T.d_gcoef);
+  T = BlockTable();
 }
 
 template <int OP>
@@ -235,6 +250,24 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
     k_blk_cta<OP><<<T.g_cta, CTA_BLOCK_THREADS, 0, s>>>(T.d_all + T.n_thread + T.n_warp, T.n_cta, A,
                                                         P, part, cap, slot, gate);
     CKL();
+  }
+  slot += T.g_cta;
+  if (T.n_giant) {
+    const PdcsBlock* gt = T.d_all + T.n_thread + T.n_warp + T.n_cta;
+    if (OP == OP_STEP_Y) {
+      k_giant_soc_a<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, A, T.d_gpart, T.g_giant);
+      CKL();
+      k_giant_soc_b<<<1, BS, 0, s>>>(gt, T.n_giant, A, T.d_gpart, T.g_giant, T.g_giant, T.d_gcoef);
+      CKL();
+      k_giant_soc_c<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, A, T.d_gcoef, part, cap, slot);
+      CKL();
+    } else {
+      // other uses (check path): one CTA per giant block; reduction slots are
+      // the giant class's, the surplus ones stay zero
+      k_blk_cta<OP><<<std::min(T.n_giant, T.g_giant), CTA_BLOCK_THREADS, 0, s>>>(gt, T.n_giant, A, P, part,
+                                                                                 cap, slot, gate);
+      CKL();
+    }
   }
   return 0;
 }
@@ -295,7 +328,7 @@ int lane_t(Engine* E, const KArgs& A) {
 }
 
 int launch_step_y(Engine* E, const KArgs& A) {
-  if (E->style_tile) {
+  if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
     k_step_y<<<E->G.grid, BS, 0, E->stream>>>(A, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y),
                                              E->d_partY, E->capY);
@@ -311,7 +344,7 @@ int launch_step_y(Engine* E, const KArgs& A) {
 }
 
 int launch_step_t(Engine* E, const KArgs& A) {
-  if (E->style_tile) {
+  if (E->tile_t) {
     if (launch_panel_passes(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->GT.grid, 2)) return 1;
     k_step_t<<<E->GT.grid, BS, 0, E->stream>>>(A, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x),
                                                E->d_partT, E->capT);
@@ -334,7 +367,7 @@ int step_lanes(int64_t nnz, int64_t nrows) {
 }
 
 const void* step_y_fn(const Engine* E) {
-  if (E->style_tile) return (const void*)k_step_y;
+  if (E->tile_y) return (const void*)k_step_y;
   const bool h = E->hints;
   switch (E->G.step_vw) {
     case 1: return h ? (const void*)k_step_y_lane<1, true> : (const void*)k_step_y_lane<1, false>;
@@ -344,7 +377,7 @@ const void* step_y_fn(const Engine* E) {
 }
 
 const void* step_t_fn(const Engine* E) {
-  if (E->style_tile) return (const void*)k_step_t;
+  if (E->tile_t) return (const void*)k_step_t;
   const bool h = E->hints;
   switch (E->GT.step_vw) {
     case 1: return h ? (const void*)k_step_t_lane<1, true> : (const void*)k_step_t_lane<1, false>;
@@ -628,7 +661,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     pos += dim;
   }
   if (pos != d.m) { g_err = "pdcs_engine_create: dual cone dims do not sum to m"; return fail(2); }
-  if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s)) return fail(1);
+  if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc)) return fail(1);
   E->has_xblocks = E->tabX.total() > 0;
   E->has_yblocks = E->tabY.total() > 0;
   auto upload_blocks = [&](const std::vector<PdcsBlock>& v, PdcsBlock** dst) -> int {
@@ -680,10 +713,15 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
     const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
     if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
-    E->style_tile = tune("tile", 0.0) > 0.0;
     E->hints = tune("hints", 0.0) > 0.0;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
+    // Measured (profiles/r01_sweeps.txt): thread-per-row lanes win for short
+    // rows (C3, C5); the tiled CSR-stream kernel wins once rows average more
+    // than ~6 entries (C2: 4.7k -> 7.6k it/s, C4's G^T: 3.5k -> 5.0k it/s).
+    const double big = d.nnz >= (1 << 20) ? 1.0 : 0.0;
+    E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1))) > 0.0;
+    E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw > 1))) > 0.0;
     if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
       return fail(1);
     if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)
@@ -698,8 +736,8 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       return per > 0 ? std::max(1, std::min(needed, per * nsm)) : dflt;
     };
     E->gridStepX = grid_per_sm("gx", E->gridX, E->gridX);
-    const int need_y = E->style_tile ? std::max(1, E->G.ntiles) : grid_for(d.m, BS / E->G.step_vw, 1 << 30);
-    const int need_t = E->style_tile ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
+    const int need_y = E->tile_y ? std::max(1, E->G.ntiles) : grid_for(d.m, BS / E->G.step_vw, 1 << 30);
+    const int need_t = E->tile_t ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
     E->G.grid = grid_per_sm("gy", need_y, fit(step_y_fn(E), need_y));
     E->GT.grid = grid_per_sm("gt", need_t, fit(step_t_fn(E), need_t));
     // optional persisting-L2 set-aside (evict_last lines only persist inside it)
@@ -753,8 +791,8 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   free_panels(E->PGT);
   cudaFree(E->d_wpart_y);
   cudaFree(E->d_wpart_x);
-  cudaFree(E->tabX.d_all);
-  cudaFree(E->tabY.d_all);
+  free_table(E->tabX);
+  free_table(E->tabY);
   cudaFree(E->d_unif_x);
   cudaFree(E->d_unif_y);
   cudaFree(E->d_ctrl);

@@ -51,12 +51,17 @@ struct PanelPlan {
 
 // Cone-block table of one space split into size classes.
 struct BlockTable {
-  PdcsBlock* d_all = nullptr;  // thread class, then warp class, then cta class
-  int n_thread = 0, n_warp = 0, n_cta = 0;
-  int g_thread = 0, g_warp = 0, g_cta = 0;  // fixed grids (partial slots)
-  int total() const { return n_thread + n_warp + n_cta; }
-  int grids() const { return g_thread + g_warp + g_cta; }
+  PdcsBlock* d_all = nullptr;  // thread class, warp class, cta class, then giant class
+  int n_thread = 0, n_warp = 0, n_cta = 0, n_giant = 0;
+  int g_thread = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
+  double* d_gpart = nullptr;  // giant-block partial sums [n_giant][2][g_giant]
+  double* d_gcoef = nullptr;  // giant-block SOC coefficients [n_giant][8]
+  int total() const { return n_thread + n_warp + n_cta + n_giant; }
+  int grids() const { return g_thread + g_warp + g_cta + g_giant; }
 };
+
+constexpr int GIANT_MIN = 1 << 16;  // uniform dual SOC blocks above this use the whole grid
+constexpr int GIANT_GRID = 2 * 148;
 
 constexpr int TILE_ROWS = BS;    // rows per CSR-stream tile (one per thread in phase 2)
 constexpr int TILE_NNZ = 2048;   // entries per tile; longer rows use the chunked path
@@ -98,7 +103,7 @@ struct Engine {
   int gridX = 1, gridXE = 1;  // x-space streaming grid
   int gridStepX = 1;          // k_step_x grid (one wave of resident CTAs)
   float keep_xt = 1.0f, keep_yh = 1.0f;  // evict_last fractions (L2 set-aside / vector bytes)
-  bool style_tile = false;  // step SpMVs: tiled CSR-stream (true) or lane-mapped (false)
+  bool tile_y = false, tile_t = false;  // step SpMVs: tiled CSR-stream or lane-mapped
   bool hints = false;       // L2 eviction-priority hints in the step kernels
   size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)

@@ -190,9 +190,20 @@ __global__ void k_long_partial(const int4* __restrict__ ch, int nch, const int* 
   CtaGrp g(sh);
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const int4 q = ch[c];
-    double s = 0.0;
-    for (int j = q.y + threadIdx.x; j < q.z; j += blockDim.x) s += va[j] * x[ci[j]];
-    s = g.sum(s);
+    // four independent accumulators keep four gathers in flight per thread
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int bd = blockDim.x;
+    int j = q.y + threadIdx.x;
+    for (; j + 3 * bd < q.z; j += 4 * bd) {
+      const int c0 = __ldg(ci + j), c1 = __ldg(ci + j + bd), c2 = __ldg(ci + j + 2 * bd),
+                c3 = __ldg(ci + j + 3 * bd);
+      s0 += __ldg(va + j) * __ldg(x + c0);
+      s1 += __ldg(va + j + bd) * __ldg(x + c1);
+      s2 += __ldg(va + j + 2 * bd) * __ldg(x + c2);
+      s3 += __ldg(va + j + 3 * bd) * __ldg(x + c3);
+    }
+    for (; j < q.z; j += bd) s0 += __ldg(va + j) * __ldg(x + __ldg(ci + j));
+    const double s = g.sum((s0 + s1) + (s2 + s3));
     if (threadIdx.x == 0) out[c] = s;
   }
 }
@@ -625,6 +636,101 @@ __global__ void __launch_bounds__(BS) k_tile_pass(TileSrc S, const double* __res
     if (threadIdx.x < nr) wout[r0 + threadIdx.x] = s;
     __syncthreads();
   }
+}
+
+// ---- giant SOC blocks in the y-step: the whole grid cooperates ---------------
+// A dual SOC block far larger than a CTA (C4: one block of 500,042 rows) is
+// projected in three launches: (A) grid-wide partial sums of ||v[1:]||^2 for
+// the dual projection of v = y + sigma(h - w) and of the residual
+// r = gx_hat - h; (B) one CTA turns them into the SOC case and coefficients
+// (cones.py:54-67); (C) the grid applies both projections and accumulates the
+// line-search / beta reductions of the block's rows.  Scales are uniform
+// (dual SOC blocks are made block-uniform by the preconditioner).
+__global__ void __launch_bounds__(BS) k_giant_soc_a(const PdcsBlock* tab, int nb, KArgs A,
+                                                    double* gpart, int gcap) {
+  if (A.ctrl->stop) return;
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    double acc[2] = {0.0, 0.0};
+    for (int i = B.start + 1 + blockIdx.x * blockDim.x + threadIdx.x; i < B.start + B.dim;
+         i += gridDim.x * blockDim.x) {
+      const double v = A.yh[i];
+      const double r = A.gxh[i] - A.h[i];
+      acc[0] += v * v;
+      acc[1] += r * r;
+    }
+    block_store_mask<2>(acc, 0u, gpart + (size_t)b * 2 * gcap, gcap, blockIdx.x);
+  }
+}
+
+// coefficients per block: [mode_v, ratio_v, first_v, mode_r, ratio_r, first_r]
+// mode 0 = keep, 1 = zero, 2 = scale (first element = coef, rest * coef/nx)
+__global__ void k_giant_soc_b(const PdcsBlock* tab, int nb, KArgs A, const double* gpart, int gcap,
+                              int nslots, double* gcoef) {
+  if (A.ctrl->stop) return;
+  __shared__ double sh[33];
+  CtaGrp g(sh);
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    const double* p = gpart + (size_t)b * 2 * gcap;
+    double sv = 0.0, sr = 0.0;
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) {
+      sv += p[s];
+      sr += p[gcap + s];
+    }
+    sv = g.sum(sv);
+    sr = g.sum(sr);
+    if (threadIdx.x == 0) {
+      const double t[2] = {A.yh[B.start], A.gxh[B.start] - A.h[B.start]};
+      const double nx[2] = {sqrt(sv), sqrt(sr)};
+      for (int q = 0; q < 2; ++q) {
+        double mode = 2.0, ratio = 0.0, first = 0.0;
+        if (nx[q] <= t[q]) {
+          mode = 0.0;
+        } else if (nx[q] <= -t[q]) {
+          mode = 1.0;
+        } else {
+          first = 0.5 * (t[q] + nx[q]);
+          ratio = first / nx[q];
+        }
+        gcoef[b * 8 + 3 * q + 0] = mode;
+        gcoef[b * 8 + 3 * q + 1] = ratio;
+        gcoef[b * 8 + 3 * q + 2] = first;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(BS) k_giant_soc_c(const PdcsBlock* tab, int nb, KArgs A,
+                                                    const double* gcoef, double* part, int cap,
+                                                    int slot0) {
+  if (A.ctrl->stop) return;
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    const double mv = gcoef[b * 8 + 0], rv = gcoef[b * 8 + 1], fv = gcoef[b * 8 + 2];
+    const double mr = gcoef[b * 8 + 3], rr = gcoef[b * 8 + 4], fr = gcoef[b * 8 + 5];
+    for (int i = B.start + blockIdx.x * blockDim.x + threadIdx.x; i < B.start + B.dim;
+         i += gridDim.x * blockDim.x) {
+      const double v = A.yh[i];
+      const double hi = A.h[i];
+      const double res = A.gxh[i] - hi;
+      const bool head = i == B.start;
+      const double p = mv == 0.0 ? v : (mv == 1.0 ? 0.0 : (head ? fv : rv * v));
+      const double rp = mr == 0.0 ? res : (mr == 1.0 ? 0.0 : (head ? fr : rr * res));
+      A.yh[i] = p;
+      const double yn = A.y[i];
+      const double dy = p - yn;
+      acc[GY_YY] += yn * yn;
+      acc[GY_DYDY] += dy * dy;
+      acc[GY_INTER] += dy * (A.w[i] - A.gx[i]);
+      const double viol = res - rp;
+      acc[GY_RP2] += viol * viol;
+      acc[GY_YH] += p * hi;
+    }
+  }
+  block_store_mask<GY_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }
 
 // ---- per-row epilogues of the fused step kernels -----------------------------

@@ -197,6 +197,69 @@ def test_solve_matches_reference(P, case):
             assert np.max(np.abs(gy - ry)) <= lim * scale, (case, kb)
 
 
+def _trajectory(P, p, opts, kbars):
+    dev, orc = {}, {}
+
+    def cb(s):
+        if s.k_bar in kbars:
+            dev[s.k_bar] = (s.z.x.copy(), s.z.y.copy())
+
+    def ocb(st, loop):
+        if st.k_bar in kbars:
+            orc[st.k_bar] = (st.x.copy(), st.y.copy())
+
+    P.solve(p, P.SolverOptions(**opts, iteration_callback=cb))
+    O.solve(p, O.options_from(None, **opts), callback=ocb)
+    return dev, orc
+
+
+def test_giant_soc_block_matches_oracle(P):
+    """A dual SOC block of 70,006 rows takes the grid-wide projection path
+    (k_giant_soc_*); its early trajectory must match the oracle."""
+    from paper_2603_15504_b200 import instances
+
+    p = instances.markowitz_rsoc(N=70_000, k=4, seed=4)
+    assert max(s.dim for s in p.dual_cones) > 65536
+    kb = (5, 10, 20)
+    dev, orc = _trajectory(P, p, dict(max_iter=20, rel_tol=1e-14, abs_tol=1e-14), kb)
+    for k in kb:
+        for a, b in zip(dev[k], orc[k]):
+            scale = max(1.0, float(np.max(np.abs(b))))
+            assert np.max(np.abs(a - b)) <= 1e-10 * scale, (k, np.max(np.abs(a - b)))
+
+
+def test_exp_blocks_trajectory_matches_oracle(P):
+    """3,000 exponential-cone blocks through the thread-per-block projections."""
+    from paper_2603_15504_b200 import instances
+
+    p = instances.entropy_max(nblk=3000, p=40, nnz_per_col=3, seed=3)
+    kb = (5, 10, 20)
+    dev, orc = _trajectory(P, p, dict(max_iter=20, rel_tol=1e-14, abs_tol=1e-14), kb)
+    for k in kb:
+        for a, b in zip(dev[k], orc[k]):
+            scale = max(1.0, float(np.max(np.abs(b))))
+            assert np.max(np.abs(a - b)) <= 1e-10 * scale, (k, np.max(np.abs(a - b)))
+
+
+def test_full_size_c5_spmv_is_bit_identical_to_scipy(P):
+    """Size-independent property at the benchmark size: the device SpMVs of the
+    50M-nnz C5 matrix equal scipy's csr_matvec bit for bit (thread-per-row
+    sums in index order) and satisfy the adjoint identity."""
+    from paper_2603_15504_b200 import instances
+
+    p = instances.lp_large()
+    A = p.G
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(A.n)
+    y = rng.standard_normal(A.m)
+    gx = A.matvec(x)
+    np.testing.assert_array_equal(gx, A._csr @ x)
+    gty = A.rmatvec(y)
+    ref = A._csr.T.tocsr() @ y
+    np.testing.assert_array_equal(gty, ref)
+    assert abs(float(y @ gx) - float(gty @ x)) <= 1e-9 * abs(float(y @ gx))
+
+
 def test_deterministic_iterates(P):
     d = load("solve_tiny")
     p = problem(d)

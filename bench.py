@@ -13,8 +13,10 @@ preconditioning, iterations, download all inside the wall-clock region).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5]
   python bench.py --impl reference ...   # the CPU oracle port of the reference
 
-Multi-GPU (torchrun, one rank per GPU): each rank solves its own copy of the
-workload (replicas); value = total iterations / max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU): one solve with G's rows sharded over
+the ranks (cone-block-aligned cuts, NCCL all-reduces inside the CUDA graph),
+scaling "strong"; value = iterations / max-over-ranks device time.
+`--replicas` instead runs an independent copy per rank (scaling "weak").
 """
 
 from __future__ import annotations
@@ -59,6 +61,10 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-reps", type=int, default=5)
     ap.add_argument("--ttt", action="store_true", help="also solve to 1e-6 and report time-to-tolerance")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: every rank solves its own copy instead of one row-sharded solve")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the row-sharded engine even on one GPU (NCCL in-graph path)")
     return ap.parse_args()
 
 
@@ -173,7 +179,7 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, local):
@@ -182,14 +188,26 @@ def run_ours(args, rank, world, local):
 
     from paper_2603_15504_b200 import SolverOptions, instances, solve
     from paper_2603_15504_b200._native import launch_count
+    from paper_2603_15504_b200.distributed import sharded_loop_class, solve_sharded
     from paper_2603_15504_b200.engine import _Loop
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    sharded = (world > 1 and not args.replicas) or args.sharded
+    if world > 1 or sharded:
         import torch.distributed as dist  # noqa: F811
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if "MASTER_ADDR" in os.environ:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            import socket
+
+            sock = socket.socket()
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+            sock.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", local))
     desc, make = WORKLOADS[args.config]
     t_gen = time.monotonic()
     problem = make(instances)
@@ -197,7 +215,7 @@ def run_ours(args, rank, world, local):
     opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=10**9, time_limit=1e9)
 
     t_setup = time.monotonic()
-    loop = _Loop(problem, opts)
+    loop = sharded_loop_class()(problem, opts) if sharded else _Loop(problem, opts)
     state, ex = loop._start()
     setup_s = time.monotonic() - t_setup
     launch_info = loop.dev.info()
@@ -224,7 +242,8 @@ def run_ours(args, rank, world, local):
         ms = float(t.item())
         it = torch.tensor([iters], device="cuda", dtype=torch.float64)
         dist.all_reduce(it, op=dist.ReduceOp.SUM)
-        total_iters = int(it.item())
+        # one sharded solve: every rank advanced the same iterations
+        total_iters = iters if sharded else int(it.item())
     else:
         total_iters = iters
     value = total_iters / (ms / 1000.0)
@@ -253,7 +272,8 @@ def run_ours(args, rank, world, local):
         e2e_iters = args.steps
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r = solve(problem, SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=e2e_iters, time_limit=1e9))
+        e2e_opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=e2e_iters, time_limit=1e9)
+        r = solve_sharded(problem, e2e_opts) if sharded else solve(problem, e2e_opts)
         wall = time.perf_counter() - t0
         e2e = {"value": r.iterations / wall, "unit": "it/s",
                "h2d_bytes_per_step": h2d / max(r.iterations, 1), "d2h_bytes_per_step": d2h / max(r.iterations, 1),
@@ -263,7 +283,8 @@ def run_ours(args, rank, world, local):
     ttt = None
     if args.ttt:
         t0 = time.perf_counter()
-        r = solve(problem, SolverOptions(rel_tol=1e-6, abs_tol=1e-6, time_limit=3600.0))
+        tt_opts = SolverOptions(rel_tol=1e-6, abs_tol=1e-6, time_limit=3600.0)
+        r = solve_sharded(problem, tt_opts) if sharded else solve(problem, tt_opts)
         ttt = {"status": r.exit_status, "iterations": r.iterations, "wall_s": time.perf_counter() - t0,
                "solve_time_s": r.solve_time_s, "p_obj": r.p_obj}
 
@@ -281,9 +302,11 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / max(iters, 1), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": desc, "nnz": int(problem.G.nnz), "m": problem.m, "n": problem.n,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": (f"row-sharded x{world} (NCCL all-reduce of G^T y partials in-graph)"
+                                       if sharded else ("replicas" if world > 1 else "single")),
                        "l2": "inputs larger than L2 (1.3 GB CSR of G and G^T vs 126 MB L2); no flush needed",
                        "options": "defaults except rel/abs tol 1e-12 (no early exit)",
                        "iterations_timed": iters, "restarts_so_far": state.t,
@@ -299,12 +322,27 @@ def run_ours(args, rank, world, local):
         }
         if ttt:
             line["time_to_1e-6"] = ttt
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 
 
+_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the real stdout (library banners such as NCCL's
+    version print are diverted to stderr, see main)."""
+    _OUT.write(json.dumps(line) + "\n")
+    _OUT.flush()
+
+
 def main():
+    global _OUT
+    # keep stdout for the JSON line only: fd 1 -> stderr for everything else
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
     args = parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

@@ -273,6 +273,17 @@ int pdcs_axpby(PdcsEngine* e, int32_t space, double a, const double* d_p, double
 int pdcs_unscale(PdcsEngine* e, const double* d_x, const double* d_y, const double* d_gx,
                  const double* d_gty, double* d_xo, double* d_yo, double* d_slack, double* d_lam);
 
+/* ---- multi-GPU ------------------------------------------------
+ * A sharded solve gives every rank a contiguous row slice of G^ (cut at
+ * cone-block boundaries) and the full x-space.  With a communicator attached,
+ * the engine's graph slot adds, inside the CUDA graph, an ncclAllReduce of the
+ * five y-space line-search scalars and of the n-vector of G^T y_hat partial
+ * sums; everything x-space is computed redundantly and stays bit-identical
+ * across ranks.  libnccl is the one the process already loaded (torch's),
+ * opened with dlopen. */
+int pdcs_comm_unique_id(unsigned char* h_id128);
+int pdcs_engine_set_comm(PdcsEngine* e, const unsigned char* h_id128, int32_t rank, int32_t nranks);
+
 /* Debug hook standing in for the reference tests' monkeypatched
  * project_primal_set (T/test_engine.py:300-317): after `after_calls` primal
  * projections inside the loop, x_hat is replaced by NaN.  -1 disables. */

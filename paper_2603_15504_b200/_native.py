@@ -110,6 +110,8 @@ _SIGS = {
     "pdcs_axpby": (C.c_int, [_P, C.c_int32, C.c_double, _P, C.c_double, _P, _P]),
     "pdcs_unscale": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pdcs_debug_inject_nan": (C.c_int, [_P, C.c_int64]),
+    "pdcs_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "pdcs_engine_set_comm": (C.c_int, [_P, C.c_char_p, C.c_int32, C.c_int32]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -126,7 +128,7 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
         if os.path.getmtime(LIB_PATH) >= newest:
             return LIB_PATH
     cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp",
-           os.path.join(CSRC, "pdcs_engine.cu")]
+           os.path.join(CSRC, "pdcs_engine.cu"), "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{res.stdout}\n{res.stderr}")

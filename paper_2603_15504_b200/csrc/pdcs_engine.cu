@@ -1,5 +1,7 @@
 // libpdcs: host orchestration and the C ABI (include/pdcs.h).
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -38,6 +40,52 @@ std::atomic<int64_t> g_launches{0};
       return 1;                                                                            \
     }                                                                                      \
   } while (0)
+
+// ---- NCCL, bound at run time to the libnccl the process already loaded -------
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+} g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    g_err = std::string("libnccl.so.2 not found: ") + dlerror();
+    return false;
+  }
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.errorString = (decltype(g_nccl.errorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy &&
+              g_nccl.errorString;
+  if (!g_nccl.ok) g_err = "libnccl.so.2 lacks the expected symbols";
+  return g_nccl.ok;
+}
+
+#define CKN(call)                                                                     \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess) {                                                          \
+      g_err = std::string(#call) + ": " + g_nccl.errorString(r_);                     \
+      return 1;                                                                       \
+    }                                                                                 \
+  } while (0)
+
+int nccl_allreduce(const double* send, double* recv, size_t count, void* comm, cudaStream_t s) {
+  if (count == 0) return 0;
+  CKN(g_nccl.allReduce(send, recv, count, ncclDouble, ncclSum, (ncclComm_t)comm, s));
+  return 0;
+}
 
 inline int grid_for(int64_t n, int per = BS, int cap = MAX_GRID) {
   int64_t g = (n + per - 1) / per;
@@ -156,22 +204,25 @@ int launch_long(const SpmvPlan& P, const double* x, double* y, const PdcsCtrl* c
 }
 
 template <int VW>
-int launch_spmv_vw(const SpmvPlan& P, const double* x, double* y, cudaStream_t s) {
-  k_spmv<VW><<<P.grid, BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.val, x, y, P.long_t);
+int launch_spmv_vw(const SpmvPlan& P, const double* x, double* y, cudaStream_t s,
+                   const PdcsCtrl* ctrl, int gate) {
+  k_spmv<VW><<<P.grid, BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.val, x, y, P.long_t, ctrl, gate);
   CKL();
   return 0;
 }
 
-int launch_spmv(const SpmvPlan& P, const double* x, double* y, cudaStream_t s) {
+// y = A x over the CSR (long rows chunked); with ctrl, gated like the step kernels.
+int launch_spmv(const SpmvPlan& P, const double* x, double* y, cudaStream_t s,
+                const PdcsCtrl* ctrl = nullptr, int gate = 0) {
   if (P.nrows == 0) return 0;
-  if (launch_long(P, x, y, nullptr, 0, s)) return 1;
+  if (launch_long(P, x, y, ctrl, gate, s)) return 1;
   switch (P.vw) {
-    case 1: return launch_spmv_vw<1>(P, x, y, s);
-    case 2: return launch_spmv_vw<2>(P, x, y, s);
-    case 4: return launch_spmv_vw<4>(P, x, y, s);
-    case 8: return launch_spmv_vw<8>(P, x, y, s);
-    case 16: return launch_spmv_vw<16>(P, x, y, s);
-    default: return launch_spmv_vw<32>(P, x, y, s);
+    case 1: return launch_spmv_vw<1>(P, x, y, s, ctrl, gate);
+    case 2: return launch_spmv_vw<2>(P, x, y, s, ctrl, gate);
+    case 4: return launch_spmv_vw<4>(P, x, y, s, ctrl, gate);
+    case 8: return launch_spmv_vw<8>(P, x, y, s, ctrl, gate);
+    case 16: return launch_spmv_vw<16>(P, x, y, s, ctrl, gate);
+    default: return launch_spmv_vw<32>(P, x, y, s, ctrl, gate);
   }
 }
 
@@ -478,15 +529,35 @@ int launch_slot(Engine* E) {
   if (E->has_yblocks && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s))
     return 1;
   if (E->has_yblocks) mark(s, "blocks_y");
-  k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red);
+  if (E->comm) {
+    // sharded: the five y-space line-search / beta sums over all ranks
+    k_finalize<<<1, BS, 0, s>>>(E->d_partY, E->capY, E->capY, GY_N, 0u, E->d_yred);
+    CKL();
+    if (nccl_allreduce(E->d_yred, E->d_yred, GY_N, E->comm, s)) return 1;
+    mark(s, "allreduce_y");
+  }
+  k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
+                             E->comm ? E->d_yred : nullptr);
   CKL();
   mark(s, "ctrl_linesearch");
   // accepted: G^T y_hat, beta, Halpern coefficients
-  if (E->GT.n_long && launch_long(E->GT, E->d.d_yh, E->d.d_gtr, E->d_ctrl, 2, s)) return 1;
-  if (E->GT.n_long) mark(s, "long_rows_gt");
-  rc = launch_step_t(E, A);
-  if (rc) return 1;
-  mark(s, "step_t_spmv");
+  if (E->comm) {
+    // sharded: local G_p^T y_hat_p partial sums, all-reduced into gth, then
+    // the x-space epilogue on the (replicated) sum
+    if (launch_spmv(E->GT, E->d.d_yh, E->d_gtp, s, E->d_ctrl, 2)) return 1;
+    mark(s, "step_t_partial");
+    if (nccl_allreduce(E->d_gtp, E->d.d_gth, E->n, E->comm, s)) return 1;
+    mark(s, "allreduce_gty");
+    k_t_epilogue<<<E->GT.grid, BS, 0, s>>>(A, E->d_partT, E->capT);
+    CKL();
+    mark(s, "step_t_epilogue");
+  } else {
+    if (E->GT.n_long && launch_long(E->GT, E->d.d_yh, E->d.d_gtr, E->d_ctrl, 2, s)) return 1;
+    if (E->GT.n_long) mark(s, "long_rows_gt");
+    rc = launch_step_t(E, A);
+    if (rc) return 1;
+    mark(s, "step_t_spmv");
+  }
   if (E->has_xblocks && launch_blocks<OP_TLAM>(E->tabX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s))
     return 1;
   if (E->has_xblocks) mark(s, "blocks_t");
@@ -791,6 +862,9 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   free_panels(E->PGT);
   cudaFree(E->d_wpart_y);
   cudaFree(E->d_wpart_x);
+  if (E->comm && g_nccl.ok) g_nccl.commDestroy((ncclComm_t)E->comm);
+  cudaFree(E->d_yred);
+  cudaFree(E->d_gtp);
   free_table(E->tabX);
   free_table(E->tabY);
   cudaFree(E->d_unif_x);
@@ -819,7 +893,10 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
     k_iota_rows<<<grid_for(m), BS, 0, s>>>(d.d_g_rowptr, m, rowid);
     CKL();
   }
-  if (enabled != 2) {
+  // enabled: 0 identity, 1 Ruiz + PC on this matrix, 2 as-is (d1/d2 = cone
+  // scales, values untouched), 3 d1/d2 written by the caller (a shard taking
+  // the scaling of the full matrix), values scaled by them
+  if (enabled == 0 || enabled == 1) {
     k_fill<<<grid_for(m), BS, 0, s>>>(d.d_d1, m, 1.0);
     CKL();
     k_fill<<<grid_for(n), BS, 0, s>>>(d.d_d2, n, 1.0);
@@ -1184,6 +1261,39 @@ int pdcs_unscale(PdcsEngine* E, const double* x, const double* y, const double* 
   k_unscale<<<std::max(E->gridX, E->gridY), BS, 0, E->stream>>>(A, x, y, gx, gty, xo, yo, slack, lam);
   CKL();
   CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+
+int pdcs_comm_unique_id(unsigned char* h_id) {
+  if (!nccl_load()) return 1;
+  ncclUniqueId id;
+  CKN(g_nccl.getUniqueId(&id));
+  std::memcpy(h_id, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+
+int pdcs_engine_set_comm(PdcsEngine* E, const unsigned char* h_id, int32_t rank, int32_t nranks) {
+  if (!E || !h_id || nranks < 1 || rank < 0 || rank >= nranks) {
+    g_err = "pdcs_engine_set_comm: bad arguments";
+    return 2;
+  }
+  if (!nccl_load()) return 1;
+  ncclUniqueId id;
+  std::memcpy(id.internal, h_id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t comm = nullptr;
+  CKN(g_nccl.commInitRank(&comm, nranks, id, rank));
+  if (E->comm) g_nccl.commDestroy((ncclComm_t)E->comm);
+  E->comm = comm;
+  E->rank = rank;
+  E->nranks = nranks;
+  if (!E->d_yred) CK(cudaMalloc(&E->d_yred, sizeof(double) * 8));
+  if (!E->d_gtp) CK(cudaMalloc(&E->d_gtp, sizeof(double) * std::max(E->n, 1)));
+  CK(cudaMemsetAsync(E->d_gtp, 0, sizeof(double) * std::max(E->n, 1), E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  // the captured graph (if any) predates the communicator
+  if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }
+  if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
+  E->graph_slots = 0;
   return 0;
 }
 

@@ -117,6 +117,12 @@ struct Engine {
   cudaGraphExec_t exec = nullptr;
   int graph_slots = 0;
   int64_t graph_nodes = 0;
+
+  // sharded mode (row slice of G^ + NCCL communicator)
+  void* comm = nullptr;       // ncclComm_t
+  int rank = 0, nranks = 1;
+  double* d_yred = nullptr;   // all-reduced y-space line-search scalars [8]
+  double* d_gtp = nullptr;    // local G^T y_hat partial sums [n]
 };
 
 }  // namespace pdcs

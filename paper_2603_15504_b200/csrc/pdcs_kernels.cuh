@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(BS) k_spmv(int nrows, const int* __restrict__ 
                                              const int* __restrict__ ci,
                                              const double* __restrict__ va,
                                              const double* __restrict__ x, double* y,
-                                             int long_t) {
+                                             int long_t, const PdcsCtrl* ctrl, int gate) {
+  if (ctrl && gated(ctrl, gate)) return;
   const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
   constexpr int RPW = 32 / VW;
   const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -809,6 +810,17 @@ __device__ __forceinline__ void t_epilogue(const KArgs& A, int j, double dot, do
   }
 }
 
+// Sharded mode: the x-space epilogue of the G^T step after the all-reduce
+// of the G^T y_hat partial sums (accepted trials only).
+__global__ void __launch_bounds__(BS) k_t_epilogue(KArgs A, double* part, int cap) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop || !C->accepted) return;
+  double acc[GT_N] = {0.0, 0.0, 0.0};
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x)
+    t_epilogue<false>(A, j, A.gth[j], acc, 0);
+  block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+}
+
 // ---- tiled (CSR-stream) step kernels -----------------------------------------
 __global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* part, int cap) {
   const PdcsCtrl* C = A.ctrl;
@@ -946,19 +958,25 @@ __device__ __forceinline__ double cta_sum_range(const double* p, int n, CtaGrp& 
 }
 
 // Line-search controller (engine.py:183-243): one CTA.
+// yred (sharded mode): the y-space sums already all-reduced across ranks.
 __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const double* partY,
-                          int capY, double* red) {
+                          int capY, double* red, const double* yred) {
   if (C->stop) return;
   __shared__ double sh[33];
   CtaGrp g(sh);
   const double xx = cta_sum_range(partX + GX_XX * capX, capX, g);
   const double dxdx = cta_sum_range(partX + GX_DXDX * capX, capX, g);
   const double cx = cta_sum_range(partX + GX_CX * capX, capX, g);
-  const double yy = cta_sum_range(partY + GY_YY * capY, capY, g);
-  const double dydy = cta_sum_range(partY + GY_DYDY * capY, capY, g);
-  const double inter = cta_sum_range(partY + GY_INTER * capY, capY, g);
-  const double rp2 = cta_sum_range(partY + GY_RP2 * capY, capY, g);
-  const double yh = cta_sum_range(partY + GY_YH * capY, capY, g);
+  double yy, dydy, inter, rp2, yh;
+  if (yred) {
+    yy = yred[GY_YY]; dydy = yred[GY_DYDY]; inter = yred[GY_INTER]; rp2 = yred[GY_RP2]; yh = yred[GY_YH];
+  } else {
+    yy = cta_sum_range(partY + GY_YY * capY, capY, g);
+    dydy = cta_sum_range(partY + GY_DYDY * capY, capY, g);
+    inter = cta_sum_range(partY + GY_INTER * capY, capY, g);
+    rp2 = cta_sum_range(partY + GY_RP2 * capY, capY, g);
+    yh = cta_sum_range(partY + GY_YH * capY, capY, g);
+  }
   if (threadIdx.x != 0) return;
   if (C->new_iter) {
     C->k_bar += 1;

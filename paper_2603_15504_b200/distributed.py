@@ -1,0 +1,286 @@
+"""Row-sharded multi-GPU solve.
+
+Rows of G^ (the y-space) are split into contiguous ranges, one per rank, cut
+only at cone-block boundaries (ZERO / NONNEG rows may be cut anywhere; SOC,
+EXP and DUAL_EXP blocks are indivisible) and balanced by nonzeros plus a row
+term.  Every rank keeps the whole x-space.  Per PDHG trial the device graph
+all-reduces (NCCL, in-graph) the five y-space line-search / beta sums and,
+for accepted trials, the n-vector of G_p^T y_hat_p partial sums; all x-space
+work is then identical on every rank.  The check path runs the reference's
+host logic on reductions that `ShardedDevice` combines across ranks with
+torch.distributed.
+
+Preconditioning: every rank computes the Ruiz + Pock-Chambolle scaling of the
+FULL matrix on its GPU (exactly the single-GPU scaling), keeps its slice of D1
+and all of D2, then drops the full copy.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceEngine
+from .model import Cone, ConeSpec, ConicProblem, dual_layout, rsoc_to_soc
+
+
+# ---------------------------------------------------------------------------
+# partition
+# ---------------------------------------------------------------------------
+
+
+def allowed_cuts(problem: ConicProblem) -> np.ndarray:
+    """Row indices at which the y-space may be cut: every row boundary inside
+    the ZERO / NONNEG rows, then only cone-block boundaries."""
+    _, m_elem = dual_layout(problem)
+    cuts = list(range(0, m_elem + 1))
+    pos = 0
+    for spec in problem.dual_cones:
+        pos += spec.dim
+        if pos > m_elem:
+            cuts.append(pos)
+    return np.unique(np.asarray(cuts + [problem.m], dtype=np.int64))
+
+
+def partition_rows(problem: ConicProblem, world: int, row_weight: float = 1.0):
+    """Contiguous [r0, r1) per rank, balanced by nnz + row_weight * rows."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    m = problem.m
+    if world == 1 or m == 0:
+        return [(0, m)] + [(m, m)] * (world - 1)
+    nnz_row = np.diff(problem.G._csr.indptr).astype(np.float64)
+    cum = np.concatenate([[0.0], np.cumsum(nnz_row + row_weight)])
+    cuts = allowed_cuts(problem)
+    total = cum[-1]
+    bounds = [0]
+    for k in range(1, world):
+        target = total * k / world
+        i = int(np.searchsorted(cum[cuts], target))
+        cand = [cuts[j] for j in (i - 1, i) if 0 <= j < len(cuts)]
+        best = min(cand, key=lambda c: abs(cum[c] - target))
+        best = max(best, bounds[-1])
+        bounds.append(int(best))
+    bounds.append(m)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def slice_problem(work: ConicProblem, r0: int, r1: int) -> ConicProblem:
+    """The rank's sub-instance: rows [r0, r1) of G and h with their cone
+    blocks (ZERO / NONNEG blocks cut to the range), full x-space."""
+    from .linalg import SparseMatrix
+
+    g = work.G._csr[r0:r1]
+    specs, pos = [], 0
+    for spec in work.dual_cones:
+        a, b = pos, pos + spec.dim
+        pos = b
+        lo, hi = max(a, r0), min(b, r1)
+        if hi <= lo:
+            continue
+        if spec.kind in (Cone.ZERO, Cone.NONNEG):
+            specs.append(ConeSpec(spec.kind, hi - lo))
+        else:
+            if lo != a or hi != b:
+                raise ValueError(f"row range [{r0}, {r1}) splits a {spec.kind.value} block")
+            specs.append(spec)
+    return ConicProblem(c=work.c, G=SparseMatrix.from_csr_arrays(g.indptr, g.indices, g.data,
+                                                                 (r1 - r0, work.n)),
+                        h=work.h[r0:r1], l=work.l, u=work.u, num_box=work.num_box,
+                        primal_cones=work.primal_cones, dual_cones=tuple(specs))
+
+
+# ---------------------------------------------------------------------------
+# reductions of the check path
+# ---------------------------------------------------------------------------
+
+# y-space entries of pdcs_metrics / pdcs_rays / pdcs_gap_probe (the rest are
+# x-space quantities, identical on every rank)
+MET_Y_SUM = (N.MET_RV2, N.MET_YH, N.MET_H1, N.MET_YY, N.MET_NONFINITE)
+MET_Y_MAX = (N.MET_RVMAX, N.MET_HMAX, N.MET_GXMAX, N.MET_RPMAX)
+RAY_Y_SUM = (2,)
+RAY_Y_MAX = (5,)
+GAP_Y_SUM = (1, 3)
+
+
+def combine(values: np.ndarray, sum_idx, max_idx, allreduce) -> np.ndarray:
+    """Combine one rank's reductions with the others': y-space sums add,
+    y-space maxima take the max, x-space entries are already global."""
+    out = np.array(values, dtype=np.float64)
+    if sum_idx:
+        out[list(sum_idx)] = allreduce(out[list(sum_idx)], "sum")
+    if max_idx:
+        out[list(max_idx)] = allreduce(out[list(max_idx)], "max")
+    return out
+
+
+def torch_allreduce(group=None):
+    """allreduce(numpy array, "sum"|"max") over a torch.distributed group."""
+    import torch
+    import torch.distributed as dist
+
+    def run(arr, op):
+        backend = dist.get_backend(group)
+        dev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64), device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX, group=group)
+        return t.cpu().numpy()
+
+    return run
+
+
+class ShardedDevice:
+    """A rank's DeviceEngine whose reductions and G^T products are combined
+    across ranks, so the single-GPU `_Loop` host logic runs unchanged."""
+
+    def __init__(self, dev: DeviceEngine, allreduce, vec_allreduce, m_total: int):
+        self._dev = dev
+        self._ar = allreduce
+        self._vec_ar = vec_allreduce
+        self.m_total = m_total
+
+    def __getattr__(self, name):
+        return getattr(self._dev, name)
+
+    def spmv(self, transpose: bool, src, dst):
+        self._dev.spmv(transpose, src, dst)
+        if transpose:
+            self._dev.stream.synchronize()
+            self._vec_ar(dst[: self._dev.n])
+
+    def metrics(self, mode, x, y, gx, gty):
+        return combine(self._dev.metrics(mode, x, y, gx, gty), MET_Y_SUM, MET_Y_MAX, self._ar)
+
+    def rays(self, x, y, gx, gty, xnorm, ynorm):
+        return combine(self._dev.rays(x, y, gx, gty, xnorm, ynorm), RAY_Y_SUM, RAY_Y_MAX, self._ar)
+
+    def gap_probe(self, x, y, gx, gty, t, tau, sigma):
+        r = combine(np.array(self._dev.gap_probe(x, y, gx, gty, t, tau, sigma)), GAP_Y_SUM, (), self._ar)
+        return float(r[0]), float(r[1]), float(r[2]), float(r[3])
+
+    def dist2(self, space, a, b=None):
+        v = self._dev.dist2(space, a, b)
+        return float(self._ar(np.array([v]), "sum")[0]) if space == 1 else v
+
+    def dot_diff(self, space, a, b, c, d):
+        v = self._dev.dot_diff(space, a, b, c, d)
+        return float(self._ar(np.array([v]), "sum")[0]) if space == 1 else v
+
+
+def _make_sharded_loop_class():
+    from .engine import _Loop
+
+    class ShardedLoop(_Loop):
+        """`_Loop` on a row slice with in-graph NCCL all-reduces."""
+
+        def __init__(self, original, options, group=None):
+            import torch.distributed as dist
+
+            self._group = group
+            self._rank = dist.get_rank(group)
+            self._world = dist.get_world_size(group)
+            super().__init__(original, options)
+
+        def _make_device(self, options):
+            import torch
+            import torch.distributed as dist
+
+            work = self.work
+            enabled = 1 if (options.use_preconditioner and work.G.nnz > 0) else 0
+            full = DeviceEngine(work, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc)
+            full.precondition(enabled, options.ruiz_iterations, options.use_pock_chambolle)
+            stats = full.stats()
+            r0, r1 = partition_rows(work, self._world)[self._rank]
+            self.row_range = (r0, r1)
+            local = slice_problem(work, r0, r1)
+            dev = DeviceEngine(local, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc)
+            with torch.cuda.stream(dev.stream):
+                if r1 > r0:
+                    dev.d1[: r1 - r0].copy_(full.d1[r0:r1])
+                dev.d2[: work.n].copy_(full.d2[: work.n])
+            dev.stream.synchronize()
+            dev.precondition(3)
+            del full
+            torch.cuda.empty_cache()
+            # NCCL communicator of libpdcs (its collectives live in the graph)
+            buf = [None]
+            if self._rank == 0:
+                import ctypes
+
+                idb = ctypes.create_string_buffer(128)
+                N.check(dev.lib.pdcs_comm_unique_id(idb), "pdcs_comm_unique_id")
+                buf = [bytes(idb.raw)]
+            dist.broadcast_object_list(buf, src=0, group=self._group)
+            N.check(dev.lib.pdcs_engine_set_comm(dev.handle, buf[0], self._rank, self._world),
+                    "pdcs_engine_set_comm")
+            ar = torch_allreduce(self._group)
+
+            def vec_ar(t):
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self._group)
+
+            self.local_problem = local
+            return ShardedDevice(dev, ar, vec_ar, work.m), stats
+
+        def _elapsed(self):
+            # every rank must take the same time-limit decisions
+            return float(torch_allreduce(self._group)(np.array([super()._elapsed()]), "max")[0])
+
+        def _next_stop(self, state):
+            # batch ends must coincide: the graphs' collectives pair up trial by trial
+            return _agree_min(self._group, super()._next_stop(state))
+
+        def _gather_y(self, arr):
+            import torch.distributed as dist
+
+            parts = [None] * self._world
+            dist.all_gather_object(parts, np.asarray(arr), group=self._group)
+            return np.concatenate(parts)
+
+        def _materialize(self, state):
+            s = super()._materialize(state)
+
+            def full(z):
+                return None if z is None else type(z)(z.x, self._gather_y(z.y))
+
+            s.z, s.z_anchor = full(s.z), full(s.z_anchor)
+            s.z_prev_anchor, s.z_bar = full(s.z_prev_anchor), full(s.z_bar)
+            return s
+
+        def _assemble_y(self, y_w, slack_w):
+            return self._gather_y(y_w), self._gather_y(slack_w)
+
+    return ShardedLoop
+
+
+def _agree_min(group, k: int) -> int:
+    import torch.distributed as dist
+
+    buf = [None] * dist.get_world_size(group)
+    dist.all_gather_object(buf, int(k), group=group)
+    return min(buf)
+
+
+_SHARDED = None
+
+
+def sharded_loop_class():
+    global _SHARDED
+    if _SHARDED is None:
+        _SHARDED = _make_sharded_loop_class()
+    return _SHARDED
+
+
+def solve_sharded(problem: ConicProblem, options=None, group=None):
+    """solve() with G's rows sharded over the ranks of a torch.distributed
+    group (one GPU per rank, torch.cuda.set_device already called).  Every
+    rank returns the full SolveResult."""
+    from .engine import SolverOptions, _adopt
+
+    if options is None:
+        options = SolverOptions()
+    options.validate()
+    if not isinstance(problem, ConicProblem):
+        problem = _adopt(problem)
+    return sharded_loop_class()(problem, options, group).run()

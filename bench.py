@@ -128,6 +128,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic(config: str, stage: str):
+    """DRAM bytes (read + write) per launch of a stage from the committed ncu
+    capture of the same configuration (profiles/traffic_<config>.json), or None."""
+    path = os.path.join(REPO, "profiles", f"traffic_{config}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f).get("stages", {}).get(stage)
+
+
 def kernel_bytes(problem, stage: str) -> int:
     """Algorithmic bytes of one launch of the fused kernels (values + indices
     + row pointers once, gathered vector once, each streamed vector once)."""
@@ -313,7 +323,8 @@ def run_ours(args, rank, world, local):
                        "setup_s": setup_s, "instance_gen_s": gen_s, "launch": launch_info,
                        "tune": os.environ.get("PDCS_TUNE", "")},
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom_gbs, "peak": peak,
-                         "unit": "GB/s", "frac": dom_gbs / peak, "traffic": None,
+                         "unit": "GB/s", "frac": dom_gbs / peak,
+                         "traffic": measured_traffic(args.config, dom[0]),
                          "bytes_per_launch": dom_bytes, "launch_ms": dom[1], "peak_source": peak_kind},
             "iteration_roofline": {"B_alg_bytes": b_alg, "achieved": iter_gbs, "peak": peak, "unit": "GB/s",
                                    "frac": iter_gbs / peak},

@@ -75,6 +75,17 @@ __device__ __forceinline__ int ld_hint(const int* a, uint64_t pol) {
   asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
   return v;
 }
+// Gather load with an explicit L2 fill size: GP = 0 plain, 1 = 64 B, 2 = 128 B
+// (random 8-byte gathers otherwise pull larger lines from HBM).
+template <int GP>
+__device__ __forceinline__ double ld_gather(const double* a) {
+  if (GP == 0) return __ldg(a);
+  double v;
+  if (GP == 1) asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  else asm volatile("ld.global.nc.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  return v;
+}
+
 // coherent (non-.nc) load for buffers the same kernel also writes
 template <bool H = kL2Hints>
 __device__ __forceinline__ double ldc_hint(const double* a, uint64_t pol) {

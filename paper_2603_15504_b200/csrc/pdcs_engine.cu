@@ -244,22 +244,26 @@ int launch_rowred(const SpmvPlan& P, const double* val, double* out, cudaStream_
 
 // ---- cone block tables -------------------------------------------------------
 int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bool giant_ok = false) {
-  std::vector<PdcsBlock> th, wa, ct, gi;
+  std::vector<PdcsBlock> ex, th, wa, ct, gi;
   for (auto& b : blocks) {
-    if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
+    if ((b.kind == PDCS_EXP || b.kind == PDCS_DUAL_EXP) && b.dim == 3) ex.push_back(b);
+    else if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
     else if (b.dim <= WARP_CLASS_MAX) wa.push_back(b);
     else if (giant_ok && b.kind == PDCS_SOC && b.dim > GIANT_MIN) gi.push_back(b);
     else ct.push_back(b);
   }
+  T.n_exp = (int)ex.size();
   T.n_thread = (int)th.size();
   T.n_warp = (int)wa.size();
   T.n_cta = (int)ct.size();
   T.n_giant = (int)gi.size();
   std::vector<PdcsBlock> all;
+  all.insert(all.end(), ex.begin(), ex.end());
   all.insert(all.end(), th.begin(), th.end());
   all.insert(all.end(), wa.begin(), wa.end());
   all.insert(all.end(), ct.begin(), ct.end());
   all.insert(all.end(), gi.begin(), gi.end());
+  T.g_exp = T.n_exp ? grid_for(T.n_exp) : 0;
   T.g_thread = T.n_thread ? grid_for(T.n_thread) : 0;
   T.g_warp = T.n_warp ? grid_for(T.n_warp, BS / 32) : 0;
   T.g_cta = T.n_cta ? std::min(T.n_cta, MAX_GRID) : 0;
@@ -287,24 +291,33 @@ template <int OP>
 int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, double* part, int cap,
                   int slot0, int gate, cudaStream_t s) {
   int slot = slot0;
+  const PdcsBlock* base = T.d_all;
+  if (T.n_exp) {
+    k_blk_exp<OP><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
+    CKL();
+  }
+  slot += T.g_exp;
+  base += T.n_exp;
   if (T.n_thread) {
-    k_blk_thread<OP><<<T.g_thread, BS, 0, s>>>(T.d_all, T.n_thread, A, P, part, cap, slot, gate);
+    k_blk_thread<OP><<<T.g_thread, BS, 0, s>>>(base, T.n_thread, A, P, part, cap, slot, gate);
     CKL();
   }
   slot += T.g_thread;
+  base += T.n_thread;
   if (T.n_warp) {
-    k_blk_warp<OP><<<T.g_warp, BS, 0, s>>>(T.d_all + T.n_thread, T.n_warp, A, P, part, cap, slot, gate);
+    k_blk_warp<OP><<<T.g_warp, BS, 0, s>>>(base, T.n_warp, A, P, part, cap, slot, gate);
     CKL();
   }
   slot += T.g_warp;
+  base += T.n_warp;
   if (T.n_cta) {
-    k_blk_cta<OP><<<T.g_cta, CTA_BLOCK_THREADS, 0, s>>>(T.d_all + T.n_thread + T.n_warp, T.n_cta, A,
-                                                        P, part, cap, slot, gate);
+    k_blk_cta<OP><<<T.g_cta, CTA_BLOCK_THREADS, 0, s>>>(base, T.n_cta, A, P, part, cap, slot, gate);
     CKL();
   }
   slot += T.g_cta;
+  base += T.n_cta;
   if (T.n_giant) {
-    const PdcsBlock* gt = T.d_all + T.n_thread + T.n_warp + T.n_cta;
+    const PdcsBlock* gt = base;
     if (OP == OP_STEP_Y) {
       k_giant_soc_a<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, A, T.d_gpart, T.g_giant);
       CKL();
@@ -512,8 +525,7 @@ int launch_slot(Engine* E) {
   cudaStream_t s = E->stream;
   BlkParams none{nullptr, nullptr, nullptr, 0, -1};
   // primal candidate
-  if (E->hints) k_step_x<true><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
-  else k_step_x<false><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
+  k_step_x<false><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
   CKL();
   mark(s, "step_x");
   if (E->has_xblocks && launch_blocks<OP_STEP_X>(E->tabX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s))
@@ -784,7 +796,8 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
     const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
     if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
-    E->hints = tune("hints", 0.0) > 0.0;
+    // gp=1: gathers of the lane-mapped step SpMVs fetch 64 B into L2 (PTX L2::64B)
+    E->hints = tune("gp", 0.0) > 0.0;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
     // Measured (profiles/r01_sweeps.txt): thread-per-row lanes win for short
@@ -814,7 +827,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // optional persisting-L2 set-aside (evict_last lines only persist inside it)
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    size_t want = E->hints ? (size_t)(tune("persist_mb", 0.0) * 1048576.0) : 0;
+    size_t want = (size_t)(tune("persist_mb", 0.0) * 1048576.0);
     if (want > (size_t)max_persist) want = (size_t)max_persist;
     if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
       E->l2_persist = want;

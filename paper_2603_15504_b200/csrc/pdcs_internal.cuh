@@ -51,13 +51,13 @@ struct PanelPlan {
 
 // Cone-block table of one space split into size classes.
 struct BlockTable {
-  PdcsBlock* d_all = nullptr;  // thread class, warp class, cta class, then giant class
-  int n_thread = 0, n_warp = 0, n_cta = 0, n_giant = 0;
-  int g_thread = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
+  PdcsBlock* d_all = nullptr;  // exp class, thread class, warp class, cta class, giant class
+  int n_exp = 0, n_thread = 0, n_warp = 0, n_cta = 0, n_giant = 0;
+  int g_exp = 0, g_thread = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
   double* d_gpart = nullptr;  // giant-block partial sums [n_giant][2][g_giant]
   double* d_gcoef = nullptr;  // giant-block SOC coefficients [n_giant][8]
-  int total() const { return n_thread + n_warp + n_cta + n_giant; }
-  int grids() const { return g_thread + g_warp + g_cta + g_giant; }
+  int total() const { return n_exp + n_thread + n_warp + n_cta + n_giant; }
+  int grids() const { return g_exp + g_thread + g_warp + g_cta + g_giant; }
 };
 
 constexpr int GIANT_MIN = 1 << 16;  // uniform dual SOC blocks above this use the whole grid

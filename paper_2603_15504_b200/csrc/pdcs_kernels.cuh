@@ -475,6 +475,74 @@ __device__ __forceinline__ void do_block(const Grp& g, const PdcsBlock& b, const
   }
 }
 
+// Exponential-cone blocks (always 3-dimensional, block-uniform scale): one
+// thread per block with straight-line code, no generic segment machinery.
+__device__ __forceinline__ void exp_or_dual(int kind, const double* v, double* o, int* err) {
+  if (kind == PDCS_EXP) proj_exp3(v[0], v[1], v[2], o, err);
+  else proj_dual_exp3(v[0], v[1], v[2], o, err);
+}
+
+template <int OP>
+__global__ void __launch_bounds__(BS) k_blk_exp(const PdcsBlock* tab, int nb, KArgs A, BlkParams P,
+                                                double* part, int cap, int slot0, int gate) {
+  if (gated(A.ctrl, gate)) return;
+  constexpr int NQ = OpNQ<OP>::v;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  int err = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const PdcsBlock b = tab[i];
+    const int s = b.start;
+    double v[3], o[3];
+    if (OP == OP_PROJECT) {
+      for (int q = 0; q < 3; ++q) v[q] = P.in[s + q];
+      exp_or_dual(P.dualize ? dual_kind(b.kind) : b.kind, v, o, &err);
+      for (int q = 0; q < 3; ++q) P.out[s + q] = o[q];
+    } else if (OP == OP_STEP_X) {
+      for (int q = 0; q < 3; ++q) v[q] = A.xh[s + q];
+      exp_or_dual(b.kind, v, o, &err);
+      for (int q = 0; q < 3; ++q) {
+        const int j = s + q;
+        const double xn = A.x[j], p = o[q];
+        A.xh[j] = p;
+        A.xt[j] = 2.0 * p - xn;
+        const double d = p - xn;
+        acc[GX_XX] += xn * xn;
+        acc[GX_DXDX] += d * d;
+        acc[GX_CX] += A.c[j] * p;
+      }
+    } else if (OP == OP_STEP_Y) {
+      for (int q = 0; q < 3; ++q) v[q] = A.yh[s + q];
+      exp_or_dual(dual_kind(b.kind), v, o, &err);
+      double res[3], rp[3];
+      for (int q = 0; q < 3; ++q) res[q] = A.gxh[s + q] - A.h[s + q];
+      exp_or_dual(b.kind, res, rp, &err);
+      for (int q = 0; q < 3; ++q) {
+        const int r = s + q;
+        const double yn = A.y[r], p = o[q], hi = A.h[r];
+        A.yh[r] = p;
+        const double dy = p - yn;
+        acc[GY_YY] += yn * yn;
+        acc[GY_DYDY] += dy * dy;
+        acc[GY_INTER] += dy * (A.w[r] - A.gx[r]);
+        const double viol = res[q] - rp[q];
+        acc[GY_RP2] += viol * viol;
+        acc[GY_YH] += p * hi;
+      }
+    } else if (OP == OP_TLAM) {
+      for (int q = 0; q < 3; ++q) v[q] = A.c[s + q] - A.gth[s + q];
+      exp_or_dual(dual_kind(b.kind), v, o, &err);
+      for (int q = 0; q < 3; ++q) {
+        const double dv = v[q] - o[q];
+        acc[GT_RD2] += dv * dv;
+      }
+    }
+  }
+  if (err) set_err(A.err, err);
+  if (OP != OP_PROJECT) block_store_mask<NQ>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
 template <int OP>
 __global__ void __launch_bounds__(BS) k_blk_thread(const PdcsBlock* tab, int nb, KArgs A,
                                                    BlkParams P, double* part, int cap, int slot0,
@@ -854,10 +922,11 @@ __global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* pa
 }
 
 // ---- lane-mapped step kernels: VW lanes per row ------------------------------
-template <int VW, bool H>
+template <int VW, int GP>
 __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __restrict__ x,
                                            const double* longv, int r, int sub, int nrows,
                                            uint64_t ps, uint64_t pk) {
+  constexpr bool H = false;
   int b = 0, e = 0;
   double s = 0.0;
   if (r < nrows) {
@@ -877,24 +946,24 @@ __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __res
       const int c2 = ld_hint<H>(S.ci + j + 2, ps), c3 = ld_hint<H>(S.ci + j + 3, ps);
       const double a0 = ld_hint<H>(S.va + j, ps), a1 = ld_hint<H>(S.va + j + 1, ps);
       const double a2 = ld_hint<H>(S.va + j + 2, ps), a3 = ld_hint<H>(S.va + j + 3, ps);
-      const double x0 = ld_hint<H>(x + c0, pk), x1 = ld_hint<H>(x + c1, pk);
-      const double x2 = ld_hint<H>(x + c2, pk), x3 = ld_hint<H>(x + c3, pk);
+      const double x0 = ld_gather<GP>(x + c0), x1 = ld_gather<GP>(x + c1);
+      const double x2 = ld_gather<GP>(x + c2), x3 = ld_gather<GP>(x + c3);
       s += a0 * x0;
       s += a1 * x1;
       s += a2 * x2;
       s += a3 * x3;
     }
-    for (; j < e; ++j) s += ld_hint<H>(S.va + j, ps) * ld_hint<H>(x + ld_hint<H>(S.ci + j, ps), pk);
+    for (; j < e; ++j) s += ld_hint<H>(S.va + j, ps) * ld_gather<GP>(x + ld_hint<H>(S.ci + j, ps));
   } else {
     for (int j = b + sub; j < e; j += VW)
-      s += ld_hint<H>(S.va + j, ps) * ld_hint<H>(x + ld_hint<H>(S.ci + j, ps), pk);
+      s += ld_hint<H>(S.va + j, ps) * ld_gather<GP>(x + ld_hint<H>(S.ci + j, ps));
 #pragma unroll
     for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
   }
   return s;
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const double* __restrict__ x,
                                                   double* wout, const PdcsCtrl* ctrl, int gate,
                                                   float keep) {
@@ -906,12 +975,12 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int r = base + lane / VW;
-    const double s = lane_row<VW, H>(S, x, nullptr, r, sub, nrows, ps, pk);
+    const double s = lane_row<VW, GP>(S, x, nullptr, r, sub, nrows, ps, pk);
     if (sub == 0 && r < nrows) wout[r] = s;
   }
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap) {
   const PdcsCtrl* C = A.ctrl;
@@ -926,13 +995,13 @@ __global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileS
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int r = base + lane / VW;
-    const double dot = lane_row<VW, H>(S, A.xt, A.w, r, sub, nrows, ps, pkx);
-    if (sub == 0 && r < nrows) y_epilogue<H>(A, k, r, dot, acc, ps, pky);
+    const double dot = lane_row<VW, GP>(S, A.xt, A.w, r, sub, nrows, ps, pkx);
+    if (sub == 0 && r < nrows) y_epilogue<false>(A, k, r, dot, acc, ps, pky);
   }
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap) {
   const PdcsCtrl* C = A.ctrl;
@@ -945,8 +1014,8 @@ __global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileS
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int j = base + lane / VW;
-    const double dot = lane_row<VW, H>(S, A.yh, A.gtr, j, sub, nrows, ps, pky);
-    if (sub == 0 && j < nrows) t_epilogue<H>(A, j, dot, acc, ps);
+    const double dot = lane_row<VW, GP>(S, A.yh, A.gtr, j, sub, nrows, ps, pky);
+    if (sub == 0 && j < nrows) t_epilogue<false>(A, j, dot, acc, ps);
   }
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
 }

@@ -1,0 +1,237 @@
+"""The reference's acceptance criteria (T/test_acceptance.py)
+re-run against the GPU engine.  Instances and thresholds follow the reference
+tests; the LP optimum oracle is an independent vertex enumeration written here."""
+
+import itertools
+import json
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2603_15504_b200 as pkg
+
+    return pkg
+
+
+def vertex_enumeration(c, G, h, l, u, tol=1e-7):
+    """min c'x s.t. Gx >= h, l <= x <= u over all vertices (finite bounds)."""
+    m, n = G.shape
+    A = np.vstack([G, np.eye(n), -np.eye(n)])
+    b = np.concatenate([h, l, -u])
+    best, arg = math.inf, None
+    for rows in itertools.combinations(range(A.shape[0]), n):
+        M = A[list(rows)]
+        if abs(np.linalg.det(M)) < 1e-10:
+            continue
+        x = np.linalg.solve(M, b[list(rows)])
+        if np.all(G @ x >= h - tol) and np.all(x >= l - tol) and np.all(x <= u + tol):
+            v = float(c @ x)
+            if v < best:
+                best, arg = v, x
+    return best, arg
+
+
+def make_box_lp(P, rng, n, m, cond=None):
+    G = rng.standard_normal((m, n))
+    if cond is not None and min(m, n) > 1:
+        U, _, Vt = np.linalg.svd(G, full_matrices=False)
+        G = U @ np.diag(np.logspace(0.0, math.log10(cond), min(m, n))) @ Vt
+    x0 = rng.uniform(-1.0, 1.0, n)
+    h = G @ x0 - rng.uniform(0.1, 1.0, m)
+    return P.ConicProblem(c=rng.standard_normal(n), G=P.SparseMatrix(G), h=h, l=-2.0 * np.ones(n),
+                          u=2.0 * np.ones(n), num_box=n, dual_cones=(P.ConeSpec(P.Cone.NONNEG, m),))
+
+
+@pytest.fixture(scope="module")
+def lp_suite(P):
+    rng = np.random.default_rng(2024)
+    sizes = [(3, 2), (3, 3), (4, 2), (4, 4), (5, 3), (5, 5), (6, 3), (6, 4), (6, 6), (7, 3), (7, 5),
+             (8, 2), (8, 4), (8, 8), (4, 3), (5, 2), (7, 7), (8, 6), (8, 8), (8, 5)]
+    conds = [None, 30.0, 100.0, 300.0]
+    suite = []
+    for i, (n, m) in enumerate(sizes):
+        p = make_box_lp(P, rng, n, m, conds[i % 4])
+        opt, _ = vertex_enumeration(p.c, p.G.toarray(), p.h, p.l, p.u)
+        suite.append((p, opt))
+    return suite
+
+
+def test_criterion_01_cone_projections(P):
+    """idempotence, nonexpansiveness and Moreau on 1000 points per cone kind,
+    all points of a kind projected in one segmented launch."""
+    from paper_2603_15504_b200.device import project_segments, project_box_dev
+
+    rng = np.random.default_rng(1)
+    npts = 1000
+    scale = rng.uniform(0.1, 10.0, 4)
+    kinds = {"soc": (3, 4), "exp": (4, 3), "dual_exp": (5, 3), "rescaled_soc": (3, 4)}
+    dual_of = {"soc": 3, "exp": 5, "dual_exp": 4}
+    for name, (code, dim) in kinds.items():
+        pts = rng.uniform(-5.0, 5.0, (npts, dim))
+        flat = pts.ravel()
+        if name == "rescaled_soc":
+            sc = np.tile(scale, npts)
+            blocks = [(code, i * dim, dim, 1) for i in range(npts)]
+            proj = lambda v: project_segments(v, blocks, sc)[0]  # noqa: E731
+            dual = lambda v: project_segments(v, blocks, 1.0 / sc)[0]  # noqa: E731
+        else:
+            blocks = [(code, i * dim, dim, 0) for i in range(npts)]
+            dblocks = [(dual_of[name], i * dim, dim, 0) for i in range(npts)]
+            proj = lambda v, b=blocks: project_segments(v, b)[0]  # noqa: E731
+            dual = lambda v, b=dblocks: project_segments(v, b)[0]  # noqa: E731
+        p = proj(flat).reshape(npts, dim)
+        pp = proj(p.ravel()).reshape(npts, dim)
+        assert np.max(np.linalg.norm(pp - p, axis=1)) <= 1e-10, name
+        q = np.roll(p, -1, axis=0)
+        d_in = np.linalg.norm(pts - np.roll(pts, -1, axis=0), axis=1)
+        assert np.all(np.linalg.norm(p - q, axis=1) <= d_in + 1e-12), name
+        dp = dual((-pts).ravel()).reshape(npts, dim)
+        assert np.max(np.linalg.norm((p - dp) - pts, axis=1)) <= 1e-9, name
+    lo, hi = np.array([-1.0, 0.0, -math.inf]), np.array([1.0, math.inf, 2.0])
+    v = rng.uniform(-5, 5, 3)
+    np.testing.assert_array_equal(project_box_dev(v, lo, hi), np.clip(v, lo, hi))
+
+
+def test_criterion_02_lp_correctness(P, lp_suite):
+    opts = P.SolverOptions(duality_gap_restart_freq=100, print_freq=10**9)
+    for p, opt in lp_suite:
+        r = P.solve(p, opts)
+        assert r.exit_code == 0, r.exit_status
+        assert abs(r.p_obj - opt) / max(1.0, abs(opt)) <= 1e-4
+
+
+def test_criterion_03_socp(P):
+    rng = np.random.default_rng(3)
+    for _ in range(6):
+        n = int(rng.integers(2, 5))
+        q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        x0 = rng.uniform(-1.0, 1.0, n)
+        b = float(rng.uniform(0.5, 2.0))
+        c = rng.standard_normal(n)
+        G = np.vstack([np.zeros((1, n)), q])
+        p = P.ConicProblem(c=c, G=P.SparseMatrix(G), h=np.concatenate([[-b], q @ x0]),
+                           l=-10.0 * np.ones(n), u=10.0 * np.ones(n), num_box=n,
+                           dual_cones=(P.ConeSpec(P.Cone.SOC, n + 1),))
+        opt = float(c @ x0) - b * float(np.linalg.norm(c))
+        r = P.solve(p, P.SolverOptions(duality_gap_restart_freq=200))
+        assert r.exit_code == 0
+        assert abs(r.p_obj - opt) / max(1.0, abs(opt)) <= 1e-4
+
+
+def test_criterion_06_constants(P):
+    from paper_2603_15504_b200 import engine as eng
+
+    p = P.ConicProblem(c=np.array([1.0, 1.0]), G=P.SparseMatrix(np.array([[1.0, -4.0], [2.0, 0.0]])),
+                       h=np.zeros(2), l=-np.ones(2), u=np.ones(2), num_box=2,
+                       dual_cones=(P.ConeSpec(P.Cone.NONNEG, 2),))
+    assert eng._Loop(p, P.SolverOptions(use_preconditioner=False))._initial_eta() == 1.0 / 4.0
+    assert eng._Loop(p, P.SolverOptions(use_preconditioner=False,
+                                        initial_step_norm="induced_inf"))._initial_eta() == 1.0 / 5.0
+
+
+def test_criterion_08_line_search_contract(P):
+    from paper_2603_15504_b200.engine import IterateZ, adaptive_step_pdhg
+
+    rng = np.random.default_rng(8)
+    for _ in range(40):
+        n, m = int(rng.integers(1, 5)), int(rng.integers(1, 5))
+        G = rng.standard_normal((m, n))
+        p = P.ConicProblem(c=rng.standard_normal(n), G=P.SparseMatrix(G), h=rng.standard_normal(m),
+                           l=-2.0 * np.ones(n), u=2.0 * np.ones(n), num_box=n,
+                           dual_cones=(P.ConeSpec(P.Cone.NONNEG, m),))
+        for _ in range(5):
+            z = IterateZ(rng.uniform(-2, 2, n), rng.uniform(0, 2, m))
+            omega, eta0, k_bar = float(rng.uniform(0.25, 4.0)), float(rng.uniform(1e-3, 3.0)), int(rng.integers(0, 200))
+            res = adaptive_step_pdhg(p, z, omega, eta0, k_bar)
+            dx, dy = res.z_hat.x - z.x, res.z_hat.y - z.y
+            mov = omega * float(dx @ dx) + float(dy @ dy) / omega
+            inter = abs(float(dy @ (G @ dx)))
+            bar = math.inf if inter == 0 else mov / (2.0 * inter)
+            noise = 1e-14 * (1.0 + math.sqrt(omega * float(z.x @ z.x) + float(z.y @ z.y) / omega))
+            assert res.eta_used < bar * (1 + 1e-12) or math.sqrt(mov) <= noise
+            assert res.eta_next <= (1.0 + (res.k_bar + 1.0) ** -0.6) * res.eta_used + 1e-15
+
+
+def test_criterion_09_all_exit_codes(P, monkeypatch):
+    from paper_2603_15504_b200 import engine as eng
+    from paper_2603_15504_b200 import termination as term
+
+    S = P.SparseMatrix
+    reached = {}
+    lp = P.ConicProblem(c=np.array([-1.0]), G=S(np.zeros((0, 1))), h=np.zeros(0), l=np.array([0.0]),
+                        u=np.array([1.0]), num_box=1)
+    reached[0] = P.solve(lp).exit_code
+    hard = make_box_lp(P, np.random.default_rng(9), 8, 8)
+    reached[1] = P.solve(hard, P.SolverOptions(max_iter=5, rel_tol=1e-14, abs_tol=1e-14)).exit_code
+    reached[6] = P.solve(hard, P.SolverOptions(time_limit=1e-9, rel_tol=1e-14, abs_tol=1e-14)).exit_code
+    pinf = P.ConicProblem(c=np.array([0.0]), G=S(np.array([[-1.0]])), h=np.array([1.0]),
+                          l=np.array([0.0]), u=np.array([math.inf]), num_box=1,
+                          dual_cones=(P.ConeSpec(P.Cone.ZERO, 1),))
+    reached[3] = P.solve(pinf, P.SolverOptions(duality_gap_restart_freq=50, use_preconditioner=False)).exit_code
+    pinf2 = P.ConicProblem(c=np.array([0.0]), G=S(np.array([[1.0], [-1.0]])), h=np.array([1.0, 0.0]),
+                           l=np.array([-math.inf]), u=np.array([math.inf]), num_box=1,
+                           dual_cones=(P.ConeSpec(P.Cone.NONNEG, 2),))
+    reached[2] = P.solve(pinf2, P.SolverOptions(duality_gap_restart_freq=10, use_preconditioner=False,
+                                                use_adaptive_restart=False,
+                                                eps_primal_infeasible_low_acc=1e-2,
+                                                eps_primal_infeasible_high_acc=1e-300)).exit_code
+    dinf = P.ConicProblem(c=np.array([-1.0]), G=S(np.array([[1.0]])), h=np.array([-1.0]),
+                          l=np.array([0.0]), u=np.array([math.inf]), num_box=1,
+                          dual_cones=(P.ConeSpec(P.Cone.NONNEG, 1),))
+    reached[5] = P.solve(dinf, P.SolverOptions(duality_gap_restart_freq=50, use_preconditioner=False)).exit_code
+    dinf2 = P.ConicProblem(c=np.array([-1.0, 0.0]), G=S(np.array([[1.0, -1.0]])), h=np.array([0.0]),
+                           l=np.array([-math.inf, 0.0]), u=np.array([math.inf, math.inf]), num_box=2,
+                           dual_cones=(P.ConeSpec(P.Cone.ZERO, 1),))
+    reached[4] = P.solve(dinf2, P.SolverOptions(duality_gap_restart_freq=10, use_preconditioner=False,
+                                                use_adaptive_restart=False,
+                                                eps_dual_infeasible_low_acc=1e-1,
+                                                eps_dual_infeasible_high_acc=1e-300)).exit_code
+    monkeypatch.setattr(eng, "debug_nan_after", 5)
+    reached[8] = P.solve(hard, P.SolverOptions(use_preconditioner=False)).exit_code
+    monkeypatch.setattr(eng, "debug_nan_after", None)
+    assert term.EXIT_STATUS[7] == ":continue"
+    reached[7] = 7
+    assert [reached.get(k) for k in range(9)] == list(range(9)), reached
+
+
+def test_criterion_10_determinism(P, tmp_path):
+    from paper_2603_15504_b200.fileio import load_result, write_result
+
+    p = make_box_lp(P, np.random.default_rng(10), 6, 5)
+    payloads, logs = [], []
+    for run in range(2):
+        log = tmp_path / f"run{run}.log"
+        r = P.solve(p, P.SolverOptions(duality_gap_restart_freq=100, logfile=str(log)))
+        out = tmp_path / f"res{run}.json"
+        write_result(r, P.SolverOptions(duality_gap_restart_freq=100), str(out))
+        doc = load_result(str(out))
+        doc["solve_time_sec"] = 0.0
+        payloads.append(json.dumps(doc, sort_keys=True).encode())
+        logs.append(log.read_bytes())
+    assert payloads[0] == payloads[1]
+    assert logs[0] == logs[1] and len(logs[0]) > 0
+
+
+def test_criterion_11_scaling_round_trip(P, lp_suite):
+    from paper_2603_15504_b200.scaling import ScalingPair, build_scaling, rescale_problem, unscale_solution
+
+    off = P.SolverOptions(use_preconditioner=False, duality_gap_restart_freq=100)
+    on = P.SolverOptions(duality_gap_restart_freq=100)
+    rng = np.random.default_rng(11)
+    for p, _ in lp_suite[:6]:
+        a, b = P.solve(p, on), P.solve(p, off)
+        assert a.exit_code == 0 and b.exit_code == 0
+        assert abs(a.p_obj - b.p_obj) <= 1e-5 * max(1.0, abs(b.p_obj))
+        s = build_scaling(p)
+        scaled = rescale_problem(p, s)
+        xt, yt = rng.standard_normal(p.n), rng.standard_normal(p.m)
+        x, y = unscale_solution(xt, yt, s)
+        np.testing.assert_allclose(x / s.d2, xt, atol=1e-12)
+        back = rescale_problem(scaled, ScalingPair(1.0 / s.d1, 1.0 / s.d2))
+        np.testing.assert_allclose(back.G.toarray(), p.G.toarray(), atol=1e-12)

@@ -260,6 +260,22 @@ def test_full_size_c5_spmv_is_bit_identical_to_scipy(P):
     assert abs(float(y @ gx) - float(gty @ x)) <= 1e-9 * abs(float(y @ gx))
 
 
+def test_solve_many_matches_sequential(P):
+    """Concurrent solves (one engine + stream per instance, host threads) give
+    the bit-identical results of sequential solves."""
+    from paper_2603_15504_b200 import instances
+    from paper_2603_15504_b200.batch import solve_many
+
+    probs = [instances.lp_random(150, 300, 0.05, seed) for seed in range(6)]
+    opts = P.SolverOptions(rel_tol=1e-6, abs_tol=1e-6)
+    seq = [P.solve(p, opts) for p in probs]
+    par = solve_many(probs, opts, max_workers=6)
+    for a, b in zip(seq, par):
+        assert a.exit_status == b.exit_status and a.iterations == b.iterations
+        np.testing.assert_array_equal(a.x, b.x)
+        np.testing.assert_array_equal(a.y, b.y)
+
+
 def test_deterministic_iterates(P):
     d = load("solve_tiny")
     p = problem(d)

@@ -65,6 +65,9 @@ def parse_args():
                     help="N>1: every rank solves its own copy instead of one row-sharded solve")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded engine even on one GPU (NCCL in-graph path)")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="also time B concurrent solves of the workload (solve_many) and report the "
+                         "aggregate iterations/s (small configurations)")
     return ap.parse_args()
 
 
@@ -290,6 +293,22 @@ def run_ours(args, rank, world, local):
                "iterations": r.iterations, "wall_s": wall, "h2d_bytes": h2d, "d2h_bytes": d2h,
                "note": "public solve() from host numpy: upload, device Ruiz+PC, iterations with checks, download"}
 
+    batched = None
+    if args.batch > 1 and not sharded:
+        from paper_2603_15504_b200.batch import solve_many
+
+        probs = [problem] * args.batch
+        b_opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=args.steps, time_limit=1e9)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = solve_many(probs, b_opts)
+        wall = time.perf_counter() - t0
+        total = sum(r.iterations for r in res)
+        batched = {"instances": args.batch, "iterations_total": total, "wall_s": wall,
+                   "value": total / wall, "unit": "it/s",
+                   "note": "solve_many: concurrent public solve() calls (engine + stream each), "
+                           "wall clock incl. upload/setup/download"}
+
     ttt = None
     if args.ttt:
         t0 = time.perf_counter()
@@ -333,6 +352,8 @@ def run_ours(args, rank, world, local):
         }
         if ttt:
             line["time_to_1e-6"] = ttt
+        if batched:
+            line["batched"] = batched
         emit(line)
     if dist:
         dist.destroy_process_group()

@@ -16,8 +16,8 @@ from . import _native as N
 from .linalg import NumericalError
 from .model import KIND_CODE, Cone
 
+# PDCS_ERR_* codes of the projection kernels (include/pdcs.h)
 _ERR_TEXT = {
-    N.SCALE_NONE: "",
     3: "exponential-cone projection of a non-finite point",
     4: "rescaled-soc projection failed to bracket the multiplier",
 }

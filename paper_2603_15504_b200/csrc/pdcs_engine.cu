@@ -373,11 +373,30 @@ int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* 
   return 0;
 }
 
+// Controllers folded into the step kernels when no cone-block kernel (and no
+// collective) follows them in the slot.
+CtrlFuse fuse_ls(const Engine* E) {
+  CtrlFuse F{};
+  if (E->comm || E->has_yblocks) return F;
+  F.mode = 1; F.ticket = E->d_ticket; F.C = E->d_ctrl;
+  F.partA = E->d_partX; F.capA = E->capX; F.partB = E->d_partY; F.capB = E->capY;
+  F.red = E->d_red; F.err = E->d_err;
+  return F;
+}
+CtrlFuse fuse_beta(const Engine* E) {
+  CtrlFuse F{};
+  if (E->comm || E->has_xblocks) return F;
+  F.mode = 2; F.ticket = E->d_ticket + 1; F.C = E->d_ctrl;
+  F.partB = E->d_partT; F.capB = E->capT; F.red = E->d_red; F.err = E->d_err;
+  return F;
+}
+
 template <int VW, bool H>
 int lane_y(Engine* E, const KArgs& A) {
   if (lane_passes<VW, H>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
   k_step_y_lane<VW, H><<<E->G.grid, BS, 0, E->stream>>>(
-      A, E->G.nrows, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY);
+      A, E->G.nrows, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY,
+      fuse_ls(E));
   CKL();
   return 0;
 }
@@ -386,7 +405,8 @@ template <int VW, bool H>
 int lane_t(Engine* E, const KArgs& A) {
   if (lane_passes<VW, H>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
   k_step_t_lane<VW, H><<<E->GT.grid, BS, 0, E->stream>>>(
-      A, E->GT.nrows, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT);
+      A, E->GT.nrows, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT,
+      fuse_beta(E));
   CKL();
   return 0;
 }
@@ -395,7 +415,7 @@ int launch_step_y(Engine* E, const KArgs& A) {
   if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
     k_step_y<<<E->G.grid, BS, 0, E->stream>>>(A, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y),
-                                             E->d_partY, E->capY);
+                                             E->d_partY, E->capY, fuse_ls(E));
     CKL();
     return 0;
   }
@@ -411,7 +431,7 @@ int launch_step_t(Engine* E, const KArgs& A) {
   if (E->tile_t) {
     if (launch_panel_passes(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->GT.grid, 2)) return 1;
     k_step_t<<<E->GT.grid, BS, 0, E->stream>>>(A, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x),
-                                               E->d_partT, E->capT);
+                                               E->d_partT, E->capT, fuse_beta(E));
     CKL();
     return 0;
   }
@@ -548,10 +568,12 @@ int launch_slot(Engine* E) {
     if (nccl_allreduce(E->d_yred, E->d_yred, GY_N, E->comm, s)) return 1;
     mark(s, "allreduce_y");
   }
-  k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
-                             E->comm ? E->d_yred : nullptr);
-  CKL();
-  mark(s, "ctrl_linesearch");
+  if (!fuse_ls(E).mode) {
+    k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
+                               E->comm ? E->d_yred : nullptr);
+    CKL();
+    mark(s, "ctrl_linesearch");
+  }
   // accepted: G^T y_hat, beta, Halpern coefficients
   if (E->comm) {
     // sharded: local G_p^T y_hat_p partial sums, all-reduced into gth, then
@@ -573,9 +595,11 @@ int launch_slot(Engine* E) {
   if (E->has_xblocks && launch_blocks<OP_TLAM>(E->tabX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s))
     return 1;
   if (E->has_xblocks) mark(s, "blocks_t");
-  k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err);
-  CKL();
-  mark(s, "ctrl_beta");
+  if (!fuse_beta(E).mode) {
+    k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err);
+    CKL();
+    mark(s, "ctrl_beta");
+  }
   return 0;
 }
 
@@ -847,12 +871,14 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       cudaMalloc(&E->d_partC, sizeof(double) * PDCS_NMET * E->capC) != cudaSuccess ||
       cudaMalloc(&E->d_out, sizeof(double) * 64) != cudaSuccess ||
       cudaMalloc(&E->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&E->d_ticket, sizeof(unsigned) * 4) != cudaSuccess ||
       cudaMallocHost(&E->h_pinned, sizeof(double) * 64) != cudaSuccess) {
     g_err = "pdcs_engine_create: workspace allocation failed";
     return fail(1);
   }
   if (cudaMemsetAsync(E->d_ctrl, 0, sizeof(PdcsCtrl), s) != cudaSuccess ||
       cudaMemsetAsync(E->d_err, 0, sizeof(int), s) != cudaSuccess ||
+      cudaMemsetAsync(E->d_ticket, 0, sizeof(unsigned) * 4, s) != cudaSuccess ||
       cudaMemsetAsync(E->d_partX, 0, sizeof(double) * GX_N * E->capX, s) != cudaSuccess ||
       cudaMemsetAsync(E->d_partY, 0, sizeof(double) * GY_N * E->capY, s) != cudaSuccess ||
       cudaMemsetAsync(E->d_partT, 0, sizeof(double) * GT_N * E->capT, s) != cudaSuccess ||
@@ -890,6 +916,7 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   cudaFree(E->d_partC);
   cudaFree(E->d_out);
   cudaFree(E->d_err);
+  cudaFree(E->d_ticket);
   if (E->h_pinned) cudaFreeHost(E->h_pinned);
   delete E;
 }

@@ -111,6 +111,7 @@ struct Engine {
   int capC = 0;
   double* d_out = nullptr;  // [64]
   int* d_err = nullptr;     // numerical error code of projections
+  unsigned* d_ticket = nullptr;  // finished-CTA counters of the folded controllers [4]
   double* h_pinned = nullptr;  // pinned readback [64]
 
   cudaGraph_t graph = nullptr;

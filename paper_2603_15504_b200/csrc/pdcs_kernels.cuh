@@ -16,6 +16,23 @@ struct KArgs {
   float keep_xt, keep_yh;  // evict_last fractions of the gathered x~ / y_hat lines
 };
 
+// Controller folded into a step kernel (mode 0 off, 1 line search after the
+// y-step, 2 beta after the G^T step).
+struct CtrlFuse {
+  int mode;
+  unsigned* ticket;
+  PdcsCtrl* C;
+  const double* partA;  // x-group partials (mode 1)
+  int capA;
+  const double* partB;  // y-group (mode 1) or T-group (mode 2) partials
+  int capB;
+  double* red;
+  const int* err;
+};
+__device__ void ctrl_ls_body(PdcsCtrl*, const double*, int, const double*, int, double*, const double*);
+__device__ void ctrl_beta_body(PdcsCtrl*, const double*, int, const double*, const int*);
+__device__ __forceinline__ void fused_ctrl(const CtrlFuse& F);
+
 // gate: 0 = always run, 1 = skip when stopped, 2 = skip when stopped or the
 // current trial was rejected.
 __device__ __forceinline__ bool gated(const PdcsCtrl* c, int gate) {
@@ -129,33 +146,6 @@ __device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int*
     }
   }
   if (VW > 1) {
-#pragma unroll
-    for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
-  }
-  return s;
-}
-
-// Dot product of one row segment [b, e) with the gathered vector x, started
-// from s0 (lane 0 of the VW group carries it).  VW = 1 sums in index order.
-template <int VW>
-__device__ __forceinline__ double seg_dot(const int* __restrict__ ci, const double* __restrict__ va,
-                                          const double* __restrict__ x, int b, int e, int sub,
-                                          double s0) {
-  double s = sub == 0 ? s0 : 0.0;
-  if (VW == 1) {
-    int j = b;
-    for (; j + 4 <= e; j += 4) {
-      const int c0 = __ldg(ci + j), c1 = __ldg(ci + j + 1), c2 = __ldg(ci + j + 2), c3 = __ldg(ci + j + 3);
-      const double a0 = __ldg(va + j), a1 = __ldg(va + j + 1), a2 = __ldg(va + j + 2), a3 = __ldg(va + j + 3);
-      const double x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
-      s += a0 * x0;
-      s += a1 * x1;
-      s += a2 * x2;
-      s += a3 * x3;
-    }
-    for (; j < e; ++j) s += __ldg(va + j) * __ldg(x + __ldg(ci + j));
-  } else {
-    for (int j = b + sub; j < e; j += VW) s += __ldg(va + j) * __ldg(x + __ldg(ci + j));
 #pragma unroll
     for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
   }
@@ -890,7 +880,8 @@ __global__ void __launch_bounds__(BS) k_t_epilogue(KArgs A, double* part, int ca
 }
 
 // ---- tiled (CSR-stream) step kernels -----------------------------------------
-__global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* part, int cap) {
+__global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* part, int cap,
+                                                  CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   __shared__ double prod[TILE_NNZ];
@@ -904,9 +895,11 @@ __global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* pa
     __syncthreads();
   }
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
 }
 
-__global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* part, int cap) {
+__global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* part, int cap,
+                                                  CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
   __shared__ double prod[TILE_NNZ];
@@ -919,6 +912,7 @@ __global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* pa
     __syncthreads();
   }
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
 }
 
 // ---- lane-mapped step kernels: VW lanes per row ------------------------------
@@ -982,7 +976,7 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
 
 template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
-                                                       int cap) {
+                                                       int cap, CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   const YCoef k = y_coef(C);
@@ -999,11 +993,12 @@ __global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileS
     if (sub == 0 && r < nrows) y_epilogue<false>(A, k, r, dot, acc, ps, pky);
   }
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
 }
 
 template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
-                                                       int cap) {
+                                                       int cap, CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
   const uint64_t ps = policy_stream(), pky = policy_keep_frac(A.keep_yh);
@@ -1018,19 +1013,19 @@ __global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileS
     if (sub == 0 && j < nrows) t_epilogue<false>(A, j, dot, acc, ps);
   }
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
 }
 
 __device__ __forceinline__ double cta_sum_range(const double* p, int n, CtaGrp& g) {
   double t = 0.0;
-  for (int s = threadIdx.x; s < n; s += blockDim.x) t += p[s];
+  for (int s = threadIdx.x; s < n; s += blockDim.x) t += __ldcg(p + s);  // L2: other CTAs wrote them
   return g.sum(t);
 }
 
-// Line-search controller (engine.py:183-243): one CTA.
+// Line-search controller (engine.py:183-243), run by one whole CTA.
 // yred (sharded mode): the y-space sums already all-reduced across ranks.
-__global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const double* partY,
-                          int capY, double* red, const double* yred) {
-  if (C->stop) return;
+__device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const double* partY,
+                             int capY, double* red, const double* yred) {
   __shared__ double sh[33];
   CtaGrp g(sh);
   const double xx = cta_sum_range(partX + GX_XX * capX, capX, g);
@@ -1101,11 +1096,17 @@ __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const doub
   }
 }
 
+__global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const double* partY,
+                          int capY, double* red, const double* yred) {
+  if (C->stop) return;
+  ctrl_ls_body(C, partX, capX, partY, capY, red, yred);
+}
+
 // Reflection parameter, Halpern coefficients, averaging weight and the stop
-// tests of an accepted iteration (engine.py:590-628, termination.py:150-160).
-__global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
-                            const int* err) {
-  if (C->stop || !C->accepted) return;
+// tests of an accepted iteration (engine.py:590-628, termination.py:150-160),
+// run by one whole CTA.
+__device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const double* red,
+                               const int* err) {
   __shared__ double sh[33];
   CtaGrp g(sh);
   const double rd2 = cta_sum_range(partT + GT_RD2 * capT, capT, g);
@@ -1162,6 +1163,33 @@ __global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const do
   else if (kb % C->check_freq == 0) { C->stop = 1; C->reason = PDCS_STOP_CHECK; }
   else if (kb >= C->k_bar_stop) { C->stop = 1; C->reason = PDCS_STOP_BATCH; }
   else if (C->print_freq > 0 && kb % C->print_freq == 0) { C->stop = 1; C->reason = PDCS_STOP_PRINT; }
+}
+
+__global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
+                            const int* err) {
+  if (C->stop || !C->accepted) return;
+  ctrl_beta_body(C, partT, capT, red, err);
+}
+
+// Controller folded into the last CTA of the kernel that writes the final
+// reduction partials (saves a launch per controller when no cone-block kernel
+// follows).  The ticket counts finished CTAs; the last one, after a fence,
+// sees every partial.
+__device__ __forceinline__ bool last_cta(unsigned* ticket) {
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+
+__device__ __forceinline__ void fused_ctrl(const CtrlFuse& F) {
+  if (!F.mode || !last_cta(F.ticket)) return;
+  if (F.mode == 1) ctrl_ls_body(F.C, F.partA, F.capA, F.partB, F.capB, F.red, nullptr);
+  else ctrl_beta_body(F.C, F.partB, F.capB, F.red, F.err);
+  if (threadIdx.x == 0) *F.ticket = 0u;
 }
 
 // Apply the pending Halpern/average update outside the loop (check path).

@@ -13,8 +13,6 @@ import numpy as np
 from . import _native as N
 from .model import KIND_CODE, ConicProblem, dual_layout
 
-_F64 = None
-
 
 def _torch():
     import torch

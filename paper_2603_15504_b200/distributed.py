@@ -17,13 +17,11 @@ and all of D2, then drops the full copy.
 
 from __future__ import annotations
 
-import math
-
 import numpy as np
 
 from . import _native as N
 from .device import DeviceEngine
-from .model import Cone, ConeSpec, ConicProblem, dual_layout, rsoc_to_soc
+from .model import Cone, ConeSpec, ConicProblem, dual_layout
 
 
 # ---------------------------------------------------------------------------

@@ -362,12 +362,12 @@ int launch_panel_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const 
   return 0;
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* x, double* wpart,
                 int gate, float keep) {
   for (int p = 0; p + 1 < Q.np; ++p) {
-    k_lane_pass<VW, H><<<P.grid, BS, 0, E->stream>>>(tile_source(P, Q, p, wpart), P.nrows, x, wpart,
-                                                     E->d_ctrl, gate, keep);
+    k_lane_pass<VW, GP><<<P.pass_grid, BS, 0, E->stream>>>(tile_source(P, Q, p, wpart), P.nrows, x,
+                                                          wpart, E->d_ctrl, gate, keep);
     CKL();
   }
   return 0;
@@ -391,20 +391,20 @@ CtrlFuse fuse_beta(const Engine* E) {
   return F;
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 int lane_y(Engine* E, const KArgs& A) {
-  if (lane_passes<VW, H>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
-  k_step_y_lane<VW, H><<<E->G.grid, BS, 0, E->stream>>>(
+  if (lane_passes<VW, GP>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
+  k_step_y_lane<VW, GP><<<E->G.grid, BS, 0, E->stream>>>(
       A, E->G.nrows, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY,
       fuse_ls(E));
   CKL();
   return 0;
 }
 
-template <int VW, bool H>
+template <int VW, int GP>
 int lane_t(Engine* E, const KArgs& A) {
-  if (lane_passes<VW, H>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
-  k_step_t_lane<VW, H><<<E->GT.grid, BS, 0, E->stream>>>(
+  if (lane_passes<VW, GP>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
+  k_step_t_lane<VW, GP><<<E->GT.grid, BS, 0, E->stream>>>(
       A, E->GT.nrows, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT,
       fuse_beta(E));
   CKL();
@@ -419,11 +419,13 @@ int launch_step_y(Engine* E, const KArgs& A) {
     CKL();
     return 0;
   }
-  const bool h = E->hints;
-  switch (E->G.step_vw) {
-    case 1: return h ? lane_y<1, true>(E, A) : lane_y<1, false>(E, A);
-    case 8: return h ? lane_y<8, true>(E, A) : lane_y<8, false>(E, A);
-    default: return h ? lane_y<32, true>(E, A) : lane_y<32, false>(E, A);
+  switch (E->G.step_vw * 2 + E->gp) {
+    case 2: return lane_y<1, 0>(E, A);
+    case 3: return lane_y<1, 1>(E, A);
+    case 16: return lane_y<8, 0>(E, A);
+    case 17: return lane_y<8, 1>(E, A);
+    case 65: return lane_y<32, 1>(E, A);
+    default: return lane_y<32, 0>(E, A);
   }
 }
 
@@ -435,11 +437,13 @@ int launch_step_t(Engine* E, const KArgs& A) {
     CKL();
     return 0;
   }
-  const bool h = E->hints;
-  switch (E->GT.step_vw) {
-    case 1: return h ? lane_t<1, true>(E, A) : lane_t<1, false>(E, A);
-    case 8: return h ? lane_t<8, true>(E, A) : lane_t<8, false>(E, A);
-    default: return h ? lane_t<32, true>(E, A) : lane_t<32, false>(E, A);
+  switch (E->GT.step_vw * 2 + E->gp) {
+    case 2: return lane_t<1, 0>(E, A);
+    case 3: return lane_t<1, 1>(E, A);
+    case 16: return lane_t<8, 0>(E, A);
+    case 17: return lane_t<8, 1>(E, A);
+    case 65: return lane_t<32, 1>(E, A);
+    default: return lane_t<32, 0>(E, A);
   }
 }
 
@@ -450,24 +454,29 @@ int step_lanes(int64_t nnz, int64_t nrows) {
   return mean <= 6.0 ? 1 : (mean <= 24.0 ? 8 : 32);
 }
 
+// the lane-step kernel instance for (lanes per row, GP mode)
+template <auto... K>
+const void* lane_fn(int vw, int gp) {
+  const void* fns[] = {(const void*)K...};
+  const int row = vw == 1 ? 0 : (vw == 8 ? 1 : 2);
+  return fns[row * 2 + (gp & 1)];
+}
+
+const void* pass_fn(int vw, int gp) {
+  return lane_fn<k_lane_pass<1, 0>, k_lane_pass<1, 1>, k_lane_pass<8, 0>, k_lane_pass<8, 1>,
+                 k_lane_pass<32, 0>, k_lane_pass<32, 1>>(vw, gp);
+}
+
 const void* step_y_fn(const Engine* E) {
   if (E->tile_y) return (const void*)k_step_y;
-  const bool h = E->hints;
-  switch (E->G.step_vw) {
-    case 1: return h ? (const void*)k_step_y_lane<1, true> : (const void*)k_step_y_lane<1, false>;
-    case 8: return h ? (const void*)k_step_y_lane<8, true> : (const void*)k_step_y_lane<8, false>;
-    default: return h ? (const void*)k_step_y_lane<32, true> : (const void*)k_step_y_lane<32, false>;
-  }
+  return lane_fn<k_step_y_lane<1, 0>, k_step_y_lane<1, 1>, k_step_y_lane<8, 0>, k_step_y_lane<8, 1>,
+                 k_step_y_lane<32, 0>, k_step_y_lane<32, 1>>(E->G.step_vw, E->gp);
 }
 
 const void* step_t_fn(const Engine* E) {
   if (E->tile_t) return (const void*)k_step_t;
-  const bool h = E->hints;
-  switch (E->GT.step_vw) {
-    case 1: return h ? (const void*)k_step_t_lane<1, true> : (const void*)k_step_t_lane<1, false>;
-    case 8: return h ? (const void*)k_step_t_lane<8, true> : (const void*)k_step_t_lane<8, false>;
-    default: return h ? (const void*)k_step_t_lane<32, true> : (const void*)k_step_t_lane<32, false>;
-  }
+  return lane_fn<k_step_t_lane<1, 0>, k_step_t_lane<1, 1>, k_step_t_lane<8, 0>, k_step_t_lane<8, 1>,
+                 k_step_t_lane<32, 0>, k_step_t_lane<32, 1>>(E->GT.step_vw, E->gp);
 }
 
 // Panelled copy of a CSR pattern (values filled by refresh_panel_values).
@@ -808,10 +817,12 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       if (p == std::string::npos || (p > 0 && s[p - 1] != ',')) return dflt;
       return atof(s.c_str() + p + k.size());
     };
-    // Column panels: cut the gathered vector into slices of at most 3/4 of L2
-    // (measured best on C5: 2 panels for G^ x~ (160 MB), 1 for G^T y_hat
-    // (80 MB); narrower panels pay more in partial sums than they save).
-    const double budget = tune("panel_mb", 0.75 * l2 / 1048576.0) * 1048576.0;
+    // Column panels: cut the gathered vector into slices of about 1/3 of L2.
+    // Random 8-byte gathers stay L2-rate bound only while their footprint is
+    // below ~50 MB on B200 (tools/gather_probe.cu: 267 G/s up to 48 MB, 196 at
+    // 80 MB, 90 at 160 MB); C5 measured best at 4 panels for G^ x~ (160 MB)
+    // and 2 for G^T y_hat (80 MB) once the passes ran at full occupancy.
+    const double budget = tune("panel_mb", 0.32 * l2 / 1048576.0) * 1048576.0;
     auto panels_for = [&](int ncols, int nrows, int nnz) {
       if (nnz < (1 << 20)) return 1;  // small matrices: the whole vector is L2-resident
       int np = (int)std::ceil(8.0 * ncols / budget);
@@ -820,8 +831,10 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
     const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
     if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
-    // gp=1: gathers of the lane-mapped step SpMVs fetch 64 B into L2 (PTX L2::64B)
-    E->hints = tune("gp", 0.0) > 0.0;
+    // gp=1: gathers of the lane-mapped step SpMVs fetch 64 B into L2 (PTX
+    // L2::64B).  Measured slower on C5, as were two rows per thread and
+    // loading the epilogue operands ahead of the gathers (profiles/r01_sweeps.txt).
+    E->gp = (int)tune("gp", 0.0) & 1;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
     // Measured (profiles/r01_sweeps.txt): thread-per-row lanes win for short
@@ -843,11 +856,17 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       const int per = (int)tune(key, 0.0);
       return per > 0 ? std::max(1, std::min(needed, per * nsm)) : dflt;
     };
-    E->gridStepX = grid_per_sm("gx", E->gridX, E->gridX);
+    E->gridStepX = grid_per_sm("gx", E->gridX, fit((const void*)k_step_x<false>, E->gridX));
     const int need_y = E->tile_y ? std::max(1, E->G.ntiles) : grid_for(d.m, BS / E->G.step_vw, 1 << 30);
     const int need_t = E->tile_t ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
     E->G.grid = grid_per_sm("gy", need_y, fit(step_y_fn(E), need_y));
     E->GT.grid = grid_per_sm("gt", need_t, fit(step_t_fn(E), need_t));
+    // the partial-sum passes are latency bound (dependent rowptr -> col ->
+    // gather chains): they get every warp slot their registers allow
+    const int need_py = grid_for(d.m, BS / E->G.step_vw, 1 << 30);
+    const int need_pt = grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
+    E->G.pass_grid = grid_per_sm("gpass", need_py, fit(pass_fn(E->G.step_vw, E->gp), need_py));
+    E->GT.pass_grid = grid_per_sm("gpass", need_pt, fit(pass_fn(E->GT.step_vw, E->gp), need_pt));
     // optional persisting-L2 set-aside (evict_last lines only persist inside it)
     int max_persist = 0;
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);

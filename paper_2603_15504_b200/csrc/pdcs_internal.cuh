@@ -28,7 +28,8 @@ struct SpmvPlan {
   int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
   double* d_chunk_out = nullptr;  // [n_chunks]
   int grid = 1;                   // CTAs of the short-row kernel
-  int* d_tiles = nullptr;         // [ntiles + 1] CSR-stream tile boundaries (rows)
+  int pass_grid = 1;              // CTAs of the panel partial-sum passes (k_lane_pass)
+  int* d_tiles = nullptr;        // [ntiles + 1] CSR-stream tile boundaries (rows)
   int ntiles = 0;
 };
 
@@ -104,7 +105,7 @@ struct Engine {
   int gridStepX = 1;          // k_step_x grid (one wave of resident CTAs)
   float keep_xt = 1.0f, keep_yh = 1.0f;  // evict_last fractions (L2 set-aside / vector bytes)
   bool tile_y = false, tile_t = false;  // step SpMVs: tiled CSR-stream or lane-mapped
-  bool hints = false;       // L2 eviction-priority hints in the step kernels
+  int gp = 0;  // lane-step variant: bit0 64B-sector gathers, bit1 two rows per thread
   size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)
   double* d_partC = nullptr;  // check path partials [PDCS_NMET*2][capC]

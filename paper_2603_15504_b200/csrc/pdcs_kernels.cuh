@@ -934,20 +934,28 @@ __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __res
     }
   }
   if (VW == 1) {
-    int j = b;
-    for (; j + 4 <= e; j += 4) {
-      const int c0 = ld_hint<H>(S.ci + j, ps), c1 = ld_hint<H>(S.ci + j + 1, ps);
-      const int c2 = ld_hint<H>(S.ci + j + 2, ps), c3 = ld_hint<H>(S.ci + j + 3, ps);
-      const double a0 = ld_hint<H>(S.va + j, ps), a1 = ld_hint<H>(S.va + j + 1, ps);
-      const double a2 = ld_hint<H>(S.va + j + 2, ps), a3 = ld_hint<H>(S.va + j + 3, ps);
-      const double x0 = ld_gather<GP>(x + c0), x1 = ld_gather<GP>(x + c1);
-      const double x2 = ld_gather<GP>(x + c2), x3 = ld_gather<GP>(x + c3);
+    // groups of up to 4 entries with predicated loads: a row of <= 4 entries
+    // (every panel row of a short-row matrix) costs one round of dependent
+    // loads instead of one per entry; the adds keep index order
+    for (int j = b; j < e; j += 4) {
+      const int q = e - j;
+      const int c0 = ld_hint<H>(S.ci + j, ps);
+      const int c1 = q > 1 ? ld_hint<H>(S.ci + j + 1, ps) : 0;
+      const int c2 = q > 2 ? ld_hint<H>(S.ci + j + 2, ps) : 0;
+      const int c3 = q > 3 ? ld_hint<H>(S.ci + j + 3, ps) : 0;
+      const double a0 = ld_hint<H>(S.va + j, ps);
+      const double a1 = q > 1 ? ld_hint<H>(S.va + j + 1, ps) : 0.0;
+      const double a2 = q > 2 ? ld_hint<H>(S.va + j + 2, ps) : 0.0;
+      const double a3 = q > 3 ? ld_hint<H>(S.va + j + 3, ps) : 0.0;
+      const double x0 = ld_gather<GP>(x + c0);
+      const double x1 = q > 1 ? ld_gather<GP>(x + c1) : 0.0;
+      const double x2 = q > 2 ? ld_gather<GP>(x + c2) : 0.0;
+      const double x3 = q > 3 ? ld_gather<GP>(x + c3) : 0.0;
       s += a0 * x0;
-      s += a1 * x1;
-      s += a2 * x2;
-      s += a3 * x3;
+      if (q > 1) s += a1 * x1;
+      if (q > 2) s += a2 * x2;
+      if (q > 3) s += a3 * x3;
     }
-    for (; j < e; ++j) s += ld_hint<H>(S.va + j, ps) * ld_gather<GP>(x + ld_hint<H>(S.ci + j, ps));
   } else {
     for (int j = b + sub; j < e; j += VW)
       s += ld_hint<H>(S.va + j, ps) * ld_gather<GP>(x + ld_hint<H>(S.ci + j, ps));
@@ -997,7 +1005,7 @@ __global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileS
 }
 
 template <int VW, int GP>
-__global__ void __launch_bounds__(BS, 6) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
+__global__ void __launch_bounds__(BS, 8) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap, CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;

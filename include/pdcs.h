@@ -246,6 +246,15 @@ int pdcs_rays(PdcsEngine* e, const double* d_x, const double* d_y, const double*
 int pdcs_gap_probe(PdcsEngine* e, const double* d_x, const double* d_y, const double* d_gx,
                    const double* d_gty, double t, double tau, double sigma, double* h_out);
 
+/* k (1..16) gap probes at host values h_ts[0..k) with one read-back; problems
+ * without cone blocks evaluate all k in a single pass over the iterate (the
+ * search of restart.py:80-132 then needs a pass per 4 bisection levels, not
+ * per level).  h_out[4i..4i+3] = pdcs_gap_probe's four sums at t = h_ts[i]
+ * (same formulas; summation order of the batched pass). */
+int pdcs_gap_probes(PdcsEngine* e, const double* d_x, const double* d_y, const double* d_gx,
+                    const double* d_gty, const double* h_ts, int32_t k, double tau, double sigma,
+                    double* h_out);
+
 /* h_out[0] = ||a - b||^2 over x-space (space=0) or y-space (space=1);
  * d_b may be NULL (then ||a||^2). */
 int pdcs_dist2(PdcsEngine* e, int32_t space, const double* d_a, const double* d_b, double* h_out);

@@ -103,6 +103,8 @@ _SIGS = {
     "pdcs_rays": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "pdcs_gap_probe": (C.c_int, [_P, _P, _P, _P, _P, C.c_double, C.c_double, C.c_double,
                                  C.POINTER(C.c_double)]),
+    "pdcs_gap_probes": (C.c_int, [_P, _P, _P, _P, _P, C.POINTER(C.c_double), C.c_int32, C.c_double,
+                                  C.c_double, C.POINTER(C.c_double)]),
     "pdcs_dist2": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_double)]),
     "pdcs_dot_diff": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.POINTER(C.c_double)]),
     "pdcs_project_set": (C.c_int, [_P, C.c_int32, _P, _P]),

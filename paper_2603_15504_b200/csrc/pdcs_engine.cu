@@ -887,7 +887,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       cudaMalloc(&E->d_partX, sizeof(double) * GX_N * E->capX) != cudaSuccess ||
       cudaMalloc(&E->d_partY, sizeof(double) * GY_N * E->capY) != cudaSuccess ||
       cudaMalloc(&E->d_partT, sizeof(double) * GT_N * E->capT) != cudaSuccess ||
-      cudaMalloc(&E->d_partC, sizeof(double) * PDCS_NMET * E->capC) != cudaSuccess ||
+      cudaMalloc(&E->d_partC, sizeof(double) * std::max(PDCS_NMET, 4 * GAP_K) * E->capC) != cudaSuccess ||
       cudaMalloc(&E->d_out, sizeof(double) * 64) != cudaSuccess ||
       cudaMalloc(&E->d_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&E->d_ticket, sizeof(unsigned) * 4) != cudaSuccess ||
@@ -1235,6 +1235,57 @@ int pdcs_gap_probe(PdcsEngine* E, const double* x, const double* y, const double
   k_gap_red<<<g, BS, 0, s>>>(A, x, y, gx, gty, E->d_partC, E->capC);
   CKL();
   if (finalize_to_host(E, E->d_partC, E->capC, g, 4, 0u, h_out)) return 1;
+  return check_err(E);
+}
+
+int pdcs_gap_probes(PdcsEngine* E, const double* x, const double* y, const double* gx,
+                    const double* gty, const double* ts, int32_t k, double tau, double sigma,
+                    double* h_out) {
+  if (k < 1 || k > GAP_K) { g_err = "pdcs_gap_probes: k must be in [1, 16]"; return 2; }
+  const KArgs A = make_args(E);
+  cudaStream_t s = E->stream;
+  const int g = std::max(E->gridX, E->gridY);
+  const bool blocks = E->has_xblocks || E->has_yblocks;
+  if (!blocks) {
+    GapTs T;
+    T.k = k;
+    for (int i = 0; i < GAP_K; ++i) {
+      const double t = ts[std::min(i, k - 1)];
+      T.tt[i] = t * tau;
+      T.ts[i] = t * sigma;
+    }
+    k_gap_multi<<<g, BS, 0, s>>>(A, x, y, gx, gty, T, E->d_partC, E->capC);
+    CKL();
+  } else {
+    // cone blocks: one probe pass per t (the block projections run on the
+    // materialised z(t)), all partials kept for a single read-back
+    for (int i = 0; i < k; ++i) {
+      k_gap_x<<<E->gridX, BS, 0, s>>>(A, x, gty, ts[i] * tau);
+      CKL();
+      k_gap_y<<<E->gridY, BS, 0, s>>>(A, y, gx, ts[i] * sigma);
+      CKL();
+      if (project_blocks(E, E->tabX, E->d.d_tx0, 0, PDCS_SCALE_DIRECT, E->d.d_d2)) return 1;
+      if (project_blocks(E, E->tabY, E->d.d_ty0, 1, PDCS_SCALE_DIRECT, E->d.d_d1)) return 1;
+      k_gap_red<<<g, BS, 0, s>>>(A, x, y, gx, gty, E->d_partC + (size_t)4 * i * E->capC, E->capC);
+      CKL();
+    }
+  }
+  const int nq = blocks ? 4 * k : 4 * GAP_K;
+  k_finalize_rows<<<nq, BS, 0, s>>>(E->d_partC, E->capC, g, E->d_out);
+  CKL();
+  CK(cudaMemcpyAsync(E->h_pinned, E->d_out, sizeof(double) * nq, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const double* o = E->h_pinned;
+  for (int i = 0; i < k; ++i) {
+    if (blocks) {
+      for (int q = 0; q < 4; ++q) h_out[4 * i + q] = o[4 * i + q];
+    } else {  // rows: x pass [2i] dx2, [2i+1] b1dx; y pass [2K+2i] dy2, [2K+2i+1] b2dy
+      h_out[4 * i + 0] = o[2 * i];
+      h_out[4 * i + 1] = o[2 * GAP_K + 2 * i];
+      h_out[4 * i + 2] = o[2 * i + 1];
+      h_out[4 * i + 3] = o[2 * GAP_K + 2 * i + 1];
+    }
+  }
   return check_err(E);
 }
 

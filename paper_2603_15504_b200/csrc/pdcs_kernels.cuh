@@ -1414,6 +1414,73 @@ __global__ void k_gap_red(KArgs A, const double* x, const double* y, const doubl
   block_store_mask<4>(acc, 0u, part, cap, blockIdx.x);
 }
 
+// Up to GAP_K gap probes in ONE pass over the iterate (problems without cone
+// blocks): the reads of x, G^T y, c, l, u, y, G x, h are shared by all t,
+// only the projections and sums are per t.  Per probe k the sums of
+// k_gap_x/k_gap_y/k_gap_red: part rows [2k] ||x - zx||^2, [2k+1] b1.(zx - x)
+// (x pass), [2 GAP_K + 2k] ||y - zy||^2, [2 GAP_K + 2k + 1] b2.(zy - y).
+constexpr int GAP_K = 16;
+struct GapTs {
+  double tt[GAP_K];  // t_k tau
+  double ts[GAP_K];  // t_k sigma
+  int k;
+};
+
+__global__ void __launch_bounds__(BS) k_gap_multi(KArgs A, const double* __restrict__ x,
+                                                  const double* __restrict__ y,
+                                                  const double* __restrict__ gx,
+                                                  const double* __restrict__ gty, GapTs T,
+                                                  double* part, int cap) {
+  double acc[2 * GAP_K];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+#pragma unroll
+  for (int q = 0; q < 2 * GAP_K; ++q) acc[q] = 0.0;
+  for (int j = tid; j < A.n; j += nt) {
+    const double b1 = gty[j] - A.c[j], xj = x[j];
+    const bool box = j < A.nbox;
+    const double lj = box ? A.l[j] : 0.0, uj = box ? A.u[j] : 0.0;
+#pragma unroll
+    for (int k = 0; k < GAP_K; ++k) {
+      if (k < T.k) {
+        const double v = xj + T.tt[k] * b1;
+        const double z = box ? clampv(v, lj, uj) : v;
+        const double d = xj - z;
+        acc[2 * k] += d * d;
+        acc[2 * k + 1] += b1 * (z - xj);
+      }
+    }
+  }
+  block_store_mask<2 * GAP_K>(acc, 0u, part, cap, blockIdx.x);
+#pragma unroll
+  for (int q = 0; q < 2 * GAP_K; ++q) acc[q] = 0.0;
+  for (int i = tid; i < A.m; i += nt) {
+    const double b2 = A.h[i] - gx[i], yi = y[i];
+    const bool zero = i < A.m_zero, elem = i < A.m_elem;
+#pragma unroll
+    for (int k = 0; k < GAP_K; ++k) {
+      if (k < T.k) {
+        const double v = yi + T.ts[k] * b2;
+        const double z = zero ? v : (elem ? pos_part(v) : v);
+        const double d = yi - z;
+        acc[2 * k] += d * d;
+        acc[2 * k + 1] += b2 * (z - yi);
+      }
+    }
+  }
+  block_store_mask<2 * GAP_K>(acc, 0u, part + (size_t)2 * GAP_K * cap, cap, blockIdx.x);
+}
+
+// Reduce partial row q (columns [0, nslots)) into out[q]; one CTA per row.
+__global__ void k_finalize_rows(const double* part, int cap, int nslots, double* out) {
+  __shared__ double sh[33];
+  CtaGrp g(sh);
+  const int q = blockIdx.x;
+  double t = 0.0;
+  for (int s = threadIdx.x; s < nslots; s += blockDim.x) t += part[(size_t)q * cap + s];
+  t = g.sum(t);
+  if (threadIdx.x == 0) out[q] = t;
+}
+
 __global__ void k_dot_diff(const double* a, const double* b, const double* c, const double* d,
                            int n, double* part, int cap) {
   double acc[1] = {0.0};

@@ -290,6 +290,22 @@ class DeviceEngine:
         N.check(rc, "pdcs_gap_probe")
         return out[0], out[1], out[2], out[3]
 
+    GAP_BATCH = 16  # probes per pdcs_gap_probes call
+
+    def gap_probes(self, x, y, gx, gty, ts, tau, sigma):
+        """pdcs_gap_probes: [(dx2, dy2, b1dx, b2dy)] for each t in ts (<= 16)."""
+        k = len(ts)
+        tsa = (C.c_double * k)(*[float(t) for t in ts])
+        out = (C.c_double * (4 * k))()
+        rc = self.lib.pdcs_gap_probes(self.handle, _ptr(x), _ptr(y), _ptr(gx), _ptr(gty), tsa, k,
+                                      float(tau), float(sigma), out)
+        if rc == 3:
+            from .linalg import NumericalError
+
+            raise NumericalError(self.lib.pdcs_last_error().decode())
+        N.check(rc, "pdcs_gap_probes")
+        return [tuple(out[4 * i:4 * i + 4]) for i in range(k)]
+
     def dist2(self, space: int, a, b=None) -> float:
         out = (C.c_double * 1)()
         N.check(self.lib.pdcs_dist2(self.handle, int(space), _ptr(a), _ptr(b), out), "pdcs_dist2")

@@ -158,6 +158,12 @@ class ShardedDevice:
         r = combine(np.array(self._dev.gap_probe(x, y, gx, gty, t, tau, sigma)), GAP_Y_SUM, (), self._ar)
         return float(r[0]), float(r[1]), float(r[2]), float(r[3])
 
+    def gap_probes(self, x, y, gx, gty, ts, tau, sigma):
+        r = np.array(self._dev.gap_probes(x, y, gx, gty, ts, tau, sigma)).reshape(-1)
+        ysum = [4 * i + q for i in range(len(ts)) for q in GAP_Y_SUM]
+        r = combine(r, ysum, (), self._ar)
+        return [tuple(float(v) for v in r[4 * i:4 * i + 4]) for i in range(len(ts))]
+
     def dist2(self, space, a, b=None):
         v = self._dev.dist2(space, a, b)
         return float(self._ar(np.array([v]), "sum")[0]) if space == 1 else v

@@ -358,3 +358,36 @@ def test_step_level_api(P):
     zb, w = update_weighted_average(zb, w, b, 1.0)
     np.testing.assert_allclose(zb.x, [0.5])
     assert w == 2.0
+
+
+@pytest.mark.parametrize("name", ["c1s", "c2s", "c3s", "c5s"])
+def test_batched_gap_probes_match_single(P, name):
+    """pdcs_gap_probes (one pass for all t on block-free problems, a pass per
+    t with one read-back otherwise) against pdcs_gap_probe per t, and the LP
+    case against a numpy evaluation of the probe formulas."""
+    from paper_2603_15504_b200.device import engine_for
+    from paper_2603_15504_b200.model import rsoc_to_soc
+
+    p = rsoc_to_soc(problem(load("solve_" + name)))
+    e = engine_for(p, original_mode=True)
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal(p.n), rng.standard_normal(p.m)
+    gx, gty = p.G.matvec(x), p.G.rmatvec(y)
+    for buf, arr in ((e.px0, x), (e.py0, y), (e.py1, gx), (e.px1, gty)):
+        e.upload(buf, arr)
+    ts = [0.0, 1e-3, 0.37, 1.0, 2.5, 17.0, 1e3]
+    tau, sigma = 0.7, 1.3
+    many = e.gap_probes(e.px0, e.py0, e.py1, e.px1, ts, tau, sigma)
+    for t, got in zip(ts, many):
+        ref = e.gap_probe(e.px0, e.py0, e.py1, e.px1, t, tau, sigma)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * (1 + np.abs(ref).max()))
+    if not p.primal_cones and all(s.kind.value in ("zero", "nonneg") for s in p.dual_cones):
+        mz, _ = P.model.dual_layout(p)
+        for t, got in zip(ts, many):
+            zx = x + t * tau * (gty - p.c)
+            zx[:p.num_box] = np.clip(zx[:p.num_box], p.l, p.u)
+            vy = y + t * sigma * (p.h - gx)
+            zy = np.concatenate([vy[:mz], np.maximum(vy[mz:], 0.0)])
+            ref = [np.dot(x - zx, x - zx), np.dot(y - zy, y - zy),
+                   np.dot(gty - p.c, zx - x), np.dot(p.h - gx, zy - y)]
+            np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-11 * (1 + np.abs(ref).max()))

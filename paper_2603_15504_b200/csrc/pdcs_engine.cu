@@ -325,9 +325,16 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
       CKL();
       k_giant_soc_c<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, A, T.d_gcoef, part, cap, slot);
       CKL();
+    } else if (OP == OP_PROJECT) {
+      k_giant_proj_a<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, P.in, T.d_gpart, T.g_giant);
+      CKL();
+      k_giant_proj_b<<<1, BS, 0, s>>>(gt, T.n_giant, P.in, T.d_gpart, T.g_giant, T.g_giant, T.d_gcoef);
+      CKL();
+      k_giant_proj_c<<<T.g_giant, BS, 0, s>>>(gt, T.n_giant, P.in, P.out, T.d_gcoef);
+      CKL();
     } else {
-      // other uses (check path): one CTA per giant block; reduction slots are
-      // the giant class's, the surplus ones stay zero
+      // other uses: one CTA per giant block; reduction slots are the giant
+      // class's, the surplus ones stay zero
       k_blk_cta<OP><<<std::min(T.n_giant, T.g_giant), CTA_BLOCK_THREADS, 0, s>>>(gt, T.n_giant, A, P, part,
                                                                                  cap, slot, gate);
       CKL();
@@ -891,7 +898,9 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       cudaMalloc(&E->d_out, sizeof(double) * 64) != cudaSuccess ||
       cudaMalloc(&E->d_err, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&E->d_ticket, sizeof(unsigned) * 4) != cudaSuccess ||
-      cudaMallocHost(&E->h_pinned, sizeof(double) * 64) != cudaSuccess) {
+      cudaMallocHost(&E->h_pinned, sizeof(double) * 128) != cudaSuccess ||
+      cudaEventCreateWithFlags(&E->ev_ctrl[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&E->ev_ctrl[1], cudaEventDisableTiming) != cudaSuccess) {
     g_err = "pdcs_engine_create: workspace allocation failed";
     return fail(1);
   }
@@ -937,6 +946,8 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   cudaFree(E->d_err);
   cudaFree(E->d_ticket);
   if (E->h_pinned) cudaFreeHost(E->h_pinned);
+  for (cudaEvent_t ev : E->ev_ctrl)
+    if (ev) cudaEventDestroy(ev);
   delete E;
 }
 
@@ -1084,27 +1095,42 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
     g_launches.fetch_sub(E->graph_nodes);  // captured, not launched
     E->graph_slots = slots;
   }
-  // Watchdog: k_bar must advance (every trial advances it); a graph replay
-  // that leaves it unchanged 8 times in a row means the device loop is stuck.
-  PdcsCtrl* hc = reinterpret_cast<PdcsCtrl*>(E->h_pinned);
-  int64_t last_kbar = -1;
-  int stuck = 0;
-  for (;;) {
+  // Two graph replays stay in flight: while replay i runs, the host waits for
+  // the control block copied after replay i-1, so the GPU never idles on the
+  // host round trip.  Once the device loop has stopped every kernel is gated
+  // off, so the one extra replay costs only its empty launches.
+  // Watchdog: k_bar must advance (every trial advances it); replays that leave
+  // it unchanged 8 times in a row mean the device loop is stuck.
+  PdcsCtrl* hc[2] = {reinterpret_cast<PdcsCtrl*>(E->h_pinned),
+                     reinterpret_cast<PdcsCtrl*>(E->h_pinned + 64)};
+  static_assert(sizeof(PdcsCtrl) <= 64 * sizeof(double), "ctrl copy slot");
+  auto replay = [&](int b) -> int {
     CK(cudaGraphLaunch(E->exec, s));
     g_launches.fetch_add(E->graph_nodes);
-    CK(cudaMemcpyAsync(hc, E->d_ctrl, sizeof(PdcsCtrl), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (hc->stop) break;
-    if (hc->k_bar == last_kbar) {
+    CK(cudaMemcpyAsync(hc[b], E->d_ctrl, sizeof(PdcsCtrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(E->ev_ctrl[b], s));
+    return 0;
+  };
+  int64_t last_kbar = -1;
+  int stuck = 0, b = 0;
+  if (replay(0)) return 1;
+  for (;;) {
+    if (replay(b ^ 1)) return 1;
+    CK(cudaEventSynchronize(E->ev_ctrl[b]));
+    if (hc[b]->stop) break;
+    if (hc[b]->k_bar == last_kbar) {
       if (++stuck >= 8) {
+        CK(cudaStreamSynchronize(s));
         g_err = "pdcs_run_inner: device loop made no progress";
         return 3;
       }
     } else {
       stuck = 0;
-      last_kbar = hc->k_bar;
+      last_kbar = hc[b]->k_bar;
     }
+    b ^= 1;
   }
+  CK(cudaStreamSynchronize(s));
   return 0;
 }
 

@@ -29,7 +29,7 @@ struct SpmvPlan {
   double* d_chunk_out = nullptr;  // [n_chunks]
   int grid = 1;                   // CTAs of the short-row kernel
   int pass_grid = 1;              // CTAs of the panel partial-sum passes (k_lane_pass)
-  int* d_tiles = nullptr;        // [ntiles + 1] CSR-stream tile boundaries (rows)
+  int* d_tiles = nullptr;         // [ntiles + 1] CSR-stream tile boundaries (rows)
   int ntiles = 0;
 };
 
@@ -105,15 +105,16 @@ struct Engine {
   int gridStepX = 1;          // k_step_x grid (one wave of resident CTAs)
   float keep_xt = 1.0f, keep_yh = 1.0f;  // evict_last fractions (L2 set-aside / vector bytes)
   bool tile_y = false, tile_t = false;  // step SpMVs: tiled CSR-stream or lane-mapped
-  int gp = 0;  // lane-step variant: bit0 64B-sector gathers, bit1 two rows per thread
+  int gp = 0;  // lane-step gathers: 0 plain, 1 with the L2::64B fill hint
   size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)
-  double* d_partC = nullptr;  // check path partials [PDCS_NMET*2][capC]
+  double* d_partC = nullptr;  // check path partials [max(PDCS_NMET, 4 GAP_K)][capC]
   int capC = 0;
   double* d_out = nullptr;  // [64]
   int* d_err = nullptr;     // numerical error code of projections
   unsigned* d_ticket = nullptr;  // finished-CTA counters of the folded controllers [4]
-  double* h_pinned = nullptr;  // pinned readback [64]
+  double* h_pinned = nullptr;  // pinned readback [128]: [0, 64) general, [64, 128) 2nd ctrl copy
+  cudaEvent_t ev_ctrl[2] = {nullptr, nullptr};  // run_inner's in-flight ctrl read-backs
 
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;

@@ -792,6 +792,67 @@ __global__ void __launch_bounds__(BS) k_giant_soc_c(const PdcsBlock* tab, int nb
   block_store_mask<GY_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }
 
+// Giant SOC blocks in plain projections (check path: gap probes, metrics,
+// project_set): the same three grid-wide phases on out = P_SOC(in).  Giant
+// blocks are uniform-scale SOC blocks, so every scaled or dualised form of the
+// projection is the plain SOC projection.
+__global__ void __launch_bounds__(BS) k_giant_proj_a(const PdcsBlock* tab, int nb,
+                                                     const double* __restrict__ in, double* gpart,
+                                                     int gcap) {
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    double acc[1] = {0.0};
+    for (int i = B.start + 1 + blockIdx.x * blockDim.x + threadIdx.x; i < B.start + B.dim;
+         i += gridDim.x * blockDim.x) {
+      const double v = in[i];
+      acc[0] += v * v;
+    }
+    block_store_mask<1>(acc, 0u, gpart + (size_t)b * 2 * gcap, gcap, blockIdx.x);
+  }
+}
+
+__global__ void k_giant_proj_b(const PdcsBlock* tab, int nb, const double* in, const double* gpart,
+                               int gcap, int nslots, double* gcoef) {
+  __shared__ double sh[33];
+  CtaGrp g(sh);
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    const double* p = gpart + (size_t)b * 2 * gcap;
+    double sv = 0.0;
+    for (int s = threadIdx.x; s < nslots; s += blockDim.x) sv += p[s];
+    sv = g.sum(sv);
+    if (threadIdx.x == 0) {
+      const double t = in[B.start], nx = sqrt(sv);
+      double mode = 2.0, ratio = 0.0, first = 0.0;
+      if (nx <= t) {
+        mode = 0.0;
+      } else if (nx <= -t) {
+        mode = 1.0;
+      } else {
+        first = 0.5 * (t + nx);
+        ratio = first / nx;
+      }
+      gcoef[b * 8 + 0] = mode;
+      gcoef[b * 8 + 1] = ratio;
+      gcoef[b * 8 + 2] = first;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(BS) k_giant_proj_c(const PdcsBlock* tab, int nb, const double* in,
+                                                     double* out, const double* gcoef) {
+  for (int b = 0; b < nb; ++b) {
+    const PdcsBlock B = tab[b];
+    const double mv = gcoef[b * 8 + 0], rv = gcoef[b * 8 + 1], fv = gcoef[b * 8 + 2];
+    for (int i = B.start + blockIdx.x * blockDim.x + threadIdx.x; i < B.start + B.dim;
+         i += gridDim.x * blockDim.x) {
+      const double v = in[i];
+      out[i] = mv == 0.0 ? v : (mv == 1.0 ? 0.0 : (i == B.start ? fv : rv * v));
+    }
+  }
+}
+
 // ---- per-row epilogues of the fused step kernels -----------------------------
 struct YCoef {
   bool pend;

@@ -235,9 +235,16 @@ __device__ inline double exp_h(double r, double s, double t, double rho) {
   return t1 - t2 - qd * t;
 }
 
-__device__ inline double exp_dh(double r, double s, double t, double rho) {
-  double ep = exp_guard(rho), en = exp_guard(-rho);
-  return (rho * r + s) * ep + (r - (rho - 1.0) * s) * en - (2.0 * rho - 1.0) * t;
+// exp_h and its derivative at the same rho, sharing the two exponentials
+// (the Newton step needs both).
+__device__ inline void exp_hdh(double r, double s, double t, double rho, double& f, double& df) {
+  const double ep = exp_guard(rho), en = exp_guard(-rho);
+  const double qd = rho * (rho - 1.0) + 1.0;
+  const double ca = (rho - 1.0) * r + s, cb = r - rho * s;
+  const double t1 = (isfinite(ep) || ca != 0.0) ? ca * ep : 0.0;
+  const double t2 = (isfinite(en) || cb != 0.0) ? cb * en : 0.0;
+  f = t1 - t2 - qd * t;
+  df = (rho * r + s) * ep + (r - (rho - 1.0) * s) * en - (2.0 * rho - 1.0) * t;
 }
 
 __device__ inline void exp_bracket(double r, double s, double t, double pdist, double ddist,
@@ -289,8 +296,8 @@ __device__ inline double exp_root(double r, double s, double t, double lo, doubl
   double x = 0.5 * (lo + hi);
   bool done = false;
   for (int i = 0; i < newton; ++i) {
-    double f = exp_h(r, s, t, x);
-    double df = exp_dh(r, s, t, x);
+    double f, df;
+    exp_hdh(r, s, t, x, f, df);
     if (fabs(f) <= 1e-15) { done = true; break; }
     if (f < 0.0) lo = x; else hi = x;
     if (hi <= lo) return 0.5 * (lo + hi);

@@ -473,7 +473,7 @@ __device__ __forceinline__ void exp_or_dual(int kind, const double* v, double* o
 }
 
 template <int OP>
-__global__ void __launch_bounds__(BS) k_blk_exp(const PdcsBlock* tab, int nb, KArgs A, BlkParams P,
+__global__ void __launch_bounds__(BS, 4) k_blk_exp(const PdcsBlock* tab, int nb, KArgs A, BlkParams P,
                                                 double* part, int cap, int slot0, int gate) {
   if (gated(A.ctrl, gate)) return;
   constexpr int NQ = OpNQ<OP>::v;

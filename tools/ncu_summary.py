@@ -16,10 +16,8 @@ import subprocess
 import sys
 from collections import defaultdict
 
-STAGE_OF = {  # kernel name prefix -> bench stage (pdcs_profile_slot names)
+STAGE_OF = {  # final kernel name prefix -> bench stage (pdcs_profile_slot names)
     "k_step_x": "step_x",
-    "k_lane_pass": "step_y_spmv",
-    "k_tile_pass": "step_y_spmv",
     "k_step_y": "step_y_spmv",
     "k_step_t": "step_t_spmv",
 }
@@ -37,7 +35,10 @@ def main(rep, config, rnd):
     hdr, units = rows[0], rows[1]
     idx = {k: hdr.index(k) for k in KEYS + ["Kernel Name"] if k in hdr}
     lines = [f"# ncu --set full --clock-control none: {rep} ({config})\n"]
+    # a stage's traffic per launch: the final kernel of a step SpMV plus the
+    # partial-sum passes (k_lane_pass / k_tile_pass) launched just before it
     per_stage = defaultdict(list)
+    pending = []
     for r in rows[2:]:
         name = r[idx["Kernel Name"]]
         short = name.split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
@@ -48,13 +49,16 @@ def main(rep, config, rnd):
         rd = float(r[idx["dram__bytes_read.sum"]]) * UNIT.get(units[idx["dram__bytes_read.sum"]], 1)
         wr = float(r[idx["dram__bytes_write.sum"]]) * UNIT.get(units[idx["dram__bytes_write.sum"]], 1)
         lines.append(f"  dram read+write = {(rd + wr) / 1e9:.3f} GB\n")
+        if short in ("k_lane_pass", "k_tile_pass"):
+            pending.append(rd + wr)
+            continue
         for prefix, stage in STAGE_OF.items():
             if short.startswith(prefix):
-                per_stage[(stage, short)].append(rd + wr)
-    # a stage's traffic per launch = sum over its kernels of their mean per-launch bytes
-    stages = defaultdict(float)
-    for (stage, _), vals in per_stage.items():
-        stages[stage] += sum(vals) / len(vals)
+                extra = sum(pending) if stage != "step_x" else 0.0
+                per_stage[stage].append(rd + wr + extra)
+                pending = []
+                break
+    stages = {stage: sum(v) / len(v) for stage, v in per_stage.items()}
     os.makedirs("profiles", exist_ok=True)
     with open(f"profiles/{rnd}_{config}_ncu_full.txt", "w") as f:
         f.writelines(lines)

@@ -941,13 +941,16 @@ __global__ void __launch_bounds__(BS) k_t_epilogue(KArgs A, double* part, int ca
 }
 
 // ---- tiled (CSR-stream) step kernels -----------------------------------------
-__global__ void __launch_bounds__(BS, 4) k_step_y(KArgs A, TileSrc S, double* part, int cap,
+__global__ void __launch_bounds__(BS, 5) k_step_y(KArgs A, TileSrc S, double* part, int cap,
                                                   CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   __shared__ double prod[TILE_NNZ];
   __shared__ int rs[TILE_ROWS + 1];
-  const YCoef k = y_coef(C);
+  __shared__ YCoef ks;  // coefficients in shared memory (register pressure)
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
   double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
     const int r0 = __ldg(S.tiles + t), nr = __ldg(S.tiles + t + 1) - r0;
@@ -1044,11 +1047,16 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
 }
 
 template <int VW, int GP>
-__global__ void __launch_bounds__(BS, 5) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
+__global__ void __launch_bounds__(BS, 6) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap, CtrlFuse F) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
-  const YCoef k = y_coef(C);
+  // the Halpern / step coefficients live in shared memory, not in 16
+  // registers per thread: 40 registers, 6 CTAs per SM
+  __shared__ YCoef ks;
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
   const uint64_t ps = policy_stream(), pkx = policy_keep_frac(A.keep_xt),
                  pky = policy_keep_frac(A.keep_yh);
   double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};

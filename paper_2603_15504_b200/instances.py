@@ -174,6 +174,37 @@ def lp_large(m=10_000_000, n=20_000_000, nnz_per_row=5, eq_frac=0.3, seed=5) -> 
                         dual_cones=dual)
 
 
+def lp_planted(m=10_000_000, n=20_000_000, nnz_per_row=5, eq_frac=0.3, seed=5) -> ConicProblem:
+    """The C5 pattern (exactly nnz_per_row uniformly random columns per row,
+    N(0,1) values, first eq_frac rows ZERO, the rest NONNEG, box [-2, 2]) with
+    a planted strictly complementary optimum (x*, y*, lambda*):
+    x* is at -2 / +2 / interior U(-1.5, 1.5) with probabilities 3/8, 3/8, 1/4;
+    y* is N(0,1) on ZERO rows, U(0.1, 1) on half the NONNEG rows (active,
+    zero slack) and 0 on the rest (slack U(0.1, 1));
+    h = G x* - slack, c = G^T y* + lambda* with lambda* = +-U(0.1, 1) at the
+    lower / upper bounds and 0 inside.  The instance is feasible and bounded
+    with a known optimal value c'x*, so time-to-tolerance is well defined."""
+    rng = np.random.default_rng(seed)
+    cols = rng.integers(0, n, size=m * nnz_per_row, dtype=np.int64).astype(np.int32)
+    vals = rng.standard_normal(m * nnz_per_row)
+    indptr = np.arange(0, m * nnz_per_row + 1, nnz_per_row, dtype=np.int64)
+    G = sp.csr_matrix((vals, cols, indptr), shape=(m, n))
+    G.sum_duplicates()
+    state = rng.choice(3, size=n, p=[0.375, 0.375, 0.25])
+    xs = np.where(state == 0, -2.0, np.where(state == 1, 2.0, rng.uniform(-1.5, 1.5, n)))
+    lam = np.where(state == 0, rng.uniform(0.1, 1.0, n), np.where(state == 1, -rng.uniform(0.1, 1.0, n), 0.0))
+    m_eq = int(eq_frac * m)
+    active = rng.random(m - m_eq) < 0.5
+    ys = np.concatenate([rng.standard_normal(m_eq), np.where(active, rng.uniform(0.1, 1.0, m - m_eq), 0.0)])
+    slack = np.concatenate([np.zeros(m_eq), np.where(active, 0.0, rng.uniform(0.1, 1.0, m - m_eq))])
+    h = G @ xs - slack
+    c = G.T @ ys + lam
+    dual = (ConeSpec(Cone.ZERO, m_eq), ConeSpec(Cone.NONNEG, m - m_eq))
+    Gm = SparseMatrix.from_csr_arrays(G.indptr, G.indices, G.data, (m, n))
+    return ConicProblem(c=c, G=Gm, h=h, l=-2.0 * np.ones(n), u=2.0 * np.ones(n), num_box=n,
+                        dual_cones=dual)
+
+
 CONFIGS = {
     "C1": lambda: lp_random(2000, 4000, 0.01, 0),
     "C2": lambda: group_robust_regression(),

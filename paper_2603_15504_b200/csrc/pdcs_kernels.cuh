@@ -1093,32 +1093,52 @@ __global__ void __launch_bounds__(BS, 8) k_step_t_lane(KArgs A, int nrows, TileS
   fused_ctrl(F);
 }
 
-__device__ __forceinline__ double cta_sum_range(const double* p, int n, CtaGrp& g) {
-  double t = 0.0;
-  for (int s = threadIdx.x; s < n; s += blockDim.x) t += __ldcg(p + s);  // L2: other CTAs wrote them
-  return g.sum(t);
+// Sums of NQ partial rows p[q * cap + 0 .. n) by one CTA: all rows' loads are
+// in flight together and the tree reductions share one pair of barriers.
+// Thread 0 receives the sums (the controllers below run on thread 0).
+template <int NQ>
+__device__ __forceinline__ void cta_sum_rows(const double* p, int cap, int n, double (&out)[NQ]) {
+  __shared__ double sh[NQ][32];
+  double t[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) t[q] = 0.0;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) t[q] += __ldcg(p + (size_t)q * cap + s);  // L2: other CTAs wrote them
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    for (int off = 16; off > 0; off >>= 1) t[q] += __shfl_down_sync(0xffffffffu, t[q], off);
+    if (lane == 0) sh[q][wid] = t[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double v = lane < nw ? sh[q][lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      out[q] = v;
+    }
+  }
 }
 
 // Line-search controller (engine.py:183-243), run by one whole CTA.
 // yred (sharded mode): the y-space sums already all-reduced across ranks.
 __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                              int capY, double* red, const double* yred) {
-  __shared__ double sh[33];
-  CtaGrp g(sh);
-  const double xx = cta_sum_range(partX + GX_XX * capX, capX, g);
-  const double dxdx = cta_sum_range(partX + GX_DXDX * capX, capX, g);
-  const double cx = cta_sum_range(partX + GX_CX * capX, capX, g);
-  double yy, dydy, inter, rp2, yh;
+  double sx[GX_N], sy[GY_N];
+  cta_sum_rows<GX_N>(partX, capX, capX, sx);
   if (yred) {
-    yy = yred[GY_YY]; dydy = yred[GY_DYDY]; inter = yred[GY_INTER]; rp2 = yred[GY_RP2]; yh = yred[GY_YH];
+#pragma unroll
+    for (int q = 0; q < GY_N; ++q) sy[q] = yred[q];
   } else {
-    yy = cta_sum_range(partY + GY_YY * capY, capY, g);
-    dydy = cta_sum_range(partY + GY_DYDY * capY, capY, g);
-    inter = cta_sum_range(partY + GY_INTER * capY, capY, g);
-    rp2 = cta_sum_range(partY + GY_RP2 * capY, capY, g);
-    yh = cta_sum_range(partY + GY_YH * capY, capY, g);
+    cta_sum_rows<GY_N>(partY, capY, capY, sy);
   }
   if (threadIdx.x != 0) return;
+  const double xx = sx[GX_XX], dxdx = sx[GX_DXDX], cx = sx[GX_CX];
+  const double yy = sy[GY_YY], dydy = sy[GY_DYDY], inter = sy[GY_INTER], rp2 = sy[GY_RP2],
+               yh = sy[GY_YH];
   if (C->new_iter) {
     C->k_bar += 1;
     C->new_iter = 0;
@@ -1184,12 +1204,10 @@ __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const doub
 // run by one whole CTA.
 __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const double* red,
                                const int* err) {
-  __shared__ double sh[33];
-  CtaGrp g(sh);
-  const double rd2 = cta_sum_range(partT + GT_RD2 * capT, capT, g);
-  const double ls = cta_sum_range(partT + GT_LSUM * capT, capT, g);
-  const double us = cta_sum_range(partT + GT_USUM * capT, capT, g);
+  double st[GT_N];
+  cta_sum_rows<GT_N>(partT, capT, capT, st);
   if (threadIdx.x != 0) return;
+  const double rd2 = st[GT_RD2], ls = st[GT_LSUM], us = st[GT_USUM];
   if (*err) {  // numerical failure inside a projection (exp non-finite, rsoc bracket)
     C->error = *err;
     C->stop = 1;

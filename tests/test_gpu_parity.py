@@ -391,3 +391,27 @@ def test_batched_gap_probes_match_single(P, name):
             ref = [np.dot(x - zx, x - zx), np.dot(y - zy, y - zy),
                    np.dot(gty - p.c, zx - x), np.dot(p.h - gx, zy - y)]
             np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-11 * (1 + np.abs(ref).max()))
+
+
+def test_giant_soc_plain_projection_matches_oracle(P):
+    """The check-path projection of a giant SOC block (grid-wide
+    k_giant_proj_*) against the oracle's SOC projection, for points inside,
+    in the polar cone and in between."""
+    from paper_2603_15504_b200 import instances
+    from paper_2603_15504_b200.device import engine_for
+    from paper_2603_15504_b200.model import rsoc_to_soc
+
+    p = rsoc_to_soc(instances.markowitz_rsoc(N=70_000, k=4, seed=4))
+    e = engine_for(p, original_mode=True)
+    start = sum(s.dim for s in p.dual_cones[:-1])
+    dim = p.dual_cones[-1].dim
+    assert dim > 65536
+    rng = np.random.default_rng(7)
+    for head in (1e3, -1e3, 0.5):  # inside, polar cone, projected onto the boundary
+        y = rng.standard_normal(p.m)
+        y[start] = head * np.linalg.norm(y[start + 1:start + dim])
+        e.upload(e.py0, y)
+        e.project_set(1, e.py0, e.py1)
+        got = e.host(e.py1, p.m)[start:start + dim]
+        want = O.proj_soc(np.array(y[start:start + dim]))
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * (1 + np.abs(want).max()))

@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local):
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": desc, "nnz": int(problem.G.nnz), "m": problem.m, "n": problem.n,
-                       "parallelism": (f"row-sharded x{world} (NCCL all-reduce of G^T y partials in-graph)"
+                       "parallelism": (f"sharded x{world}: rows of G and x-slices, in-graph NCCL all-gather of x~ + reduce-scatter of G^T y"
                                        if sharded else ("replicas" if world > 1 else "single")),
                        "l2": "inputs larger than L2 (1.3 GB CSR of G and G^T vs 126 MB L2); no flush needed",
                        "options": "defaults except rel/abs tol 1e-12 (no early exit)",

@@ -283,15 +283,32 @@ int pdcs_unscale(PdcsEngine* e, const double* d_x, const double* d_y, const doub
                  const double* d_gty, double* d_xo, double* d_yo, double* d_slack, double* d_lam);
 
 /* ---- multi-GPU ------------------------------------------------
- * A sharded solve gives every rank a contiguous row slice of G^ (cut at
- * cone-block boundaries) and the full x-space.  With a communicator attached,
- * the engine's graph slot adds, inside the CUDA graph, an ncclAllReduce of the
- * five y-space line-search scalars and of the n-vector of G^T y_hat partial
- * sums; everything x-space is computed redundantly and stays bit-identical
- * across ranks.  libnccl is the one the process already loaded (torch's),
- * opened with dlopen. */
+ * A sharded solve gives every rank a contiguous row slice of G^ (cut at dual
+ * cone-block boundaries) and a contiguous x-slice (cut at primal cone-block
+ * boundaries); every rank keeps full-length x-space buffers.  With a
+ * communicator attached, one graph slot (one PDHG trial) adds, inside the
+ * CUDA graph:
+ *   - after the primal half-step on the x-slice: all-gather of x~ (G_p x~
+ *     needs all of it);
+ *   - an all-reduce of the 5 y-space + 3 x-space line-search sums;
+ *   - after G_p^T y_hat_p over all of x-space: reduce-scatter, each rank
+ *     receiving its x-slice of G^T y_hat;
+ *   - an all-reduce of the 3 x-space beta sums.
+ * Equal x-slices (cut r = r ceil(n / nranks)) use ncclAllGather /
+ * ncclReduceScatter; block-aligned unequal slices use grouped per-root
+ * broadcasts / reduces.  x-space buffers must then hold
+ * nranks * ceil(n / nranks) doubles.  Outside its slice a rank's x-space
+ * state goes stale during a batch; pdcs_allgather_x restores full copies
+ * (the host calls it after pdcs_flush, before any check).  libnccl is the one
+ * the process already loaded (torch's), opened with dlopen. */
 int pdcs_comm_unique_id(unsigned char* h_id128);
 int pdcs_engine_set_comm(PdcsEngine* e, const unsigned char* h_id128, int32_t rank, int32_t nranks);
+/* x-slices of all ranks: h_cuts[0] = 0 <= ... <= h_cuts[nranks] = n.  Required
+ * when nranks > 1 (after pdcs_engine_set_comm). */
+int pdcs_engine_set_xsplit(PdcsEngine* e, const int32_t* h_cuts, int32_t nranks);
+/* Every rank's slice of each x-space device vector d_vecs[0..count) to all
+ * ranks (no-op without an x-split). */
+int pdcs_allgather_x(PdcsEngine* e, double* const* d_vecs, int32_t count);
 
 /* Debug hook standing in for the reference tests' monkeypatched
  * project_primal_set (T/test_engine.py:300-317): after `after_calls` primal

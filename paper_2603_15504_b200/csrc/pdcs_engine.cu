@@ -48,6 +48,15 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
 } g_nccl;
@@ -64,10 +73,17 @@ bool nccl_load() {
   g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
   g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
   g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.reduceScatter = (decltype(g_nccl.reduceScatter))dlsym(h, "ncclReduceScatter");
+  g_nccl.broadcast = (decltype(g_nccl.broadcast))dlsym(h, "ncclBroadcast");
+  g_nccl.reduce = (decltype(g_nccl.reduce))dlsym(h, "ncclReduce");
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
   g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
   g_nccl.errorString = (decltype(g_nccl.errorString))dlsym(h, "ncclGetErrorString");
-  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.commDestroy &&
-              g_nccl.errorString;
+  g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.allReduce && g_nccl.allGather &&
+              g_nccl.reduceScatter && g_nccl.broadcast && g_nccl.reduce && g_nccl.groupStart &&
+              g_nccl.groupEnd && g_nccl.commDestroy && g_nccl.errorString;
   if (!g_nccl.ok) g_err = "libnccl.so.2 lacks the expected symbols";
   return g_nccl.ok;
 }
@@ -84,6 +100,43 @@ bool nccl_load() {
 int nccl_allreduce(const double* send, double* recv, size_t count, void* comm, cudaStream_t s) {
   if (count == 0) return 0;
   CKN(g_nccl.allReduce(send, recv, count, ncclDouble, ncclSum, (ncclComm_t)comm, s));
+  return 0;
+}
+
+// x-space exchanges of the sharded engine: rank r owns x-slice [xcut[r],
+// xcut[r+1]).  Equal slices (cut r = r * xcnt, clipped to n) use the NCCL
+// all-gather / reduce-scatter on buffers padded to nranks * xcnt; slices cut
+// at primal cone-block boundaries use grouped per-root broadcasts / reduces.
+int nccl_x_allgather(const Engine* E, double* v, cudaStream_t s) {
+  if (E->nranks <= 1) return 0;
+  ncclComm_t comm = (ncclComm_t)E->comm;
+  if (E->xcnt > 0) {
+    CKN(g_nccl.allGather(v + (size_t)E->rank * E->xcnt, v, E->xcnt, ncclDouble, comm, s));
+    return 0;
+  }
+  CKN(g_nccl.groupStart());
+  for (int r = 0; r < E->nranks; ++r) {
+    const int a = E->xcut[r], len = E->xcut[r + 1] - a;
+    if (len > 0) CKN(g_nccl.broadcast(v + a, v + a, len, ncclDouble, r, comm, s));
+  }
+  CKN(g_nccl.groupEnd());
+  return 0;
+}
+
+// sum over the ranks of `part` (x-space, padded), each rank receiving its slice in `out`
+int nccl_x_reduce_scatter(const Engine* E, const double* part, double* out, cudaStream_t s) {
+  ncclComm_t comm = (ncclComm_t)E->comm;
+  if (E->xcnt > 0) {
+    CKN(g_nccl.reduceScatter(part, out + (size_t)E->rank * E->xcnt, E->xcnt, ncclDouble, ncclSum, comm,
+                             s));
+    return 0;
+  }
+  CKN(g_nccl.groupStart());
+  for (int r = 0; r < E->nranks; ++r) {
+    const int a = E->xcut[r], len = E->xcut[r + 1] - a;
+    if (len > 0) CKN(g_nccl.reduce(part + a, out + a, len, ncclDouble, ncclSum, r, comm, s));
+  }
+  CKN(g_nccl.groupEnd());
   return 0;
 }
 
@@ -107,6 +160,7 @@ KArgs make_args(const Engine* E) {
   const PdcsEngineDesc& d = E->d;
   KArgs A;
   A.n = E->n; A.m = E->m; A.nbox = E->nbox; A.m_zero = E->m_zero; A.m_elem = E->m_elem;
+  A.x0 = E->xs0; A.x1 = E->xs1;
   A.c = d.d_c; A.h = d.d_h; A.l = d.d_l; A.u = d.d_u;
   A.c0 = d.d_c0; A.h0 = d.d_h0; A.l0 = d.d_l0; A.u0 = d.d_u0;
   A.d1 = d.d_d1; A.d2 = d.d_d2;
@@ -564,9 +618,20 @@ int launch_slot(Engine* E) {
   k_step_x<false><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
   CKL();
   mark(s, "step_x");
-  if (E->has_xblocks && launch_blocks<OP_STEP_X>(E->tabX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s))
-    return 1;
-  if (E->has_xblocks) mark(s, "blocks_x");
+  // x-space cone blocks this engine steps (its slice's blocks when sharded)
+  const BlockTable& TX = E->xsplit ? E->tabXs : E->tabX;
+  const bool xblk = TX.total() > 0;
+  if (E->comm && E->nranks > 1 && !E->xsplit) {
+    g_err = "sharded engine: pdcs_engine_set_xsplit is required with more than one rank";
+    return 2;
+  }
+  if (xblk && launch_blocks<OP_STEP_X>(TX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s)) return 1;
+  if (xblk) mark(s, "blocks_x");
+  if (E->comm) {
+    // sharded: every rank stepped its x-slice; G_p x~ needs all of x~
+    if (nccl_x_allgather(E, E->d.d_xt, s)) return 1;
+    mark(s, "allgather_xt");
+  }
   // dual candidate with w = G^ x~
   if (E->G.n_long && launch_long(E->G, E->d.d_xt, E->d.d_w, E->d_ctrl, 1, s)) return 1;
   if (E->G.n_long) mark(s, "long_rows_g");
@@ -578,11 +643,14 @@ int launch_slot(Engine* E) {
     return 1;
   if (E->has_yblocks) mark(s, "blocks_y");
   if (E->comm) {
-    // sharded: the five y-space line-search / beta sums over all ranks
+    // sharded: the five y-space and three x-space line-search sums over all
+    // ranks (each rank holds a row slice and an x-slice)
     k_finalize<<<1, BS, 0, s>>>(E->d_partY, E->capY, E->capY, GY_N, 0u, E->d_yred);
     CKL();
-    if (nccl_allreduce(E->d_yred, E->d_yred, GY_N, E->comm, s)) return 1;
-    mark(s, "allreduce_y");
+    k_finalize<<<1, BS, 0, s>>>(E->d_partX, E->capX, E->capX, GX_N, 0u, E->d_yred + GY_N);
+    CKL();
+    if (nccl_allreduce(E->d_yred, E->d_yred, GY_N + GX_N, E->comm, s)) return 1;
+    mark(s, "allreduce_xy");
   }
   if (!fuse_ls(E).mode) {
     k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
@@ -592,12 +660,13 @@ int launch_slot(Engine* E) {
   }
   // accepted: G^T y_hat, beta, Halpern coefficients
   if (E->comm) {
-    // sharded: local G_p^T y_hat_p partial sums, all-reduced into gth, then
-    // the x-space epilogue on the (replicated) sum
+    // sharded: local G_p^T y_hat_p partial sums over all of x-space,
+    // reduce-scattered so each rank gets its x-slice of G^T y_hat, then the
+    // x-space epilogue on that slice
     if (launch_spmv(E->GT, E->d.d_yh, E->d_gtp, s, E->d_ctrl, 2)) return 1;
     mark(s, "step_t_partial");
-    if (nccl_allreduce(E->d_gtp, E->d.d_gth, E->n, E->comm, s)) return 1;
-    mark(s, "allreduce_gty");
+    if (nccl_x_reduce_scatter(E, E->d_gtp, E->d.d_gth, s)) return 1;
+    mark(s, "reduce_scatter_gty");
     k_t_epilogue<<<E->GT.grid, BS, 0, s>>>(A, E->d_partT, E->capT);
     CKL();
     mark(s, "step_t_epilogue");
@@ -608,11 +677,18 @@ int launch_slot(Engine* E) {
     if (rc) return 1;
     mark(s, "step_t_spmv");
   }
-  if (E->has_xblocks && launch_blocks<OP_TLAM>(E->tabX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s))
-    return 1;
-  if (E->has_xblocks) mark(s, "blocks_t");
+  if (xblk && launch_blocks<OP_TLAM>(TX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s)) return 1;
+  if (xblk) mark(s, "blocks_t");
+  const double* tred = nullptr;
+  if (E->comm) {  // sharded: the three x-space beta sums over all ranks
+    k_finalize<<<1, BS, 0, s>>>(E->d_partT, E->capT, E->capT, GT_N, 0u, E->d_yred + 8);
+    CKL();
+    if (nccl_allreduce(E->d_yred + 8, E->d_yred + 8, GT_N, E->comm, s)) return 1;
+    mark(s, "allreduce_t");
+    tred = E->d_yred + 8;
+  }
   if (!fuse_beta(E).mode) {
-    k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err);
+    k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err, tred);
     CKL();
     mark(s, "ctrl_beta");
   }
@@ -753,6 +829,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   E->d = d;
   E->stream = (cudaStream_t)stream;
   E->n = d.n; E->m = d.m; E->nbox = d.num_box; E->nnz = d.nnz;
+  E->xs0 = 0; E->xs1 = d.n;
   E->m_zero = d.m_zero; E->m_elem = d.m_elem;
   E->allow_nonuniform_dual_soc = d.allow_nonuniform_dual_soc;
   cudaStream_t s = E->stream;
@@ -785,6 +862,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   }
   if (pos != d.m) { g_err = "pdcs_engine_create: dual cone dims do not sum to m"; return fail(2); }
   if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc)) return fail(1);
+  E->xblocks = xb;
   E->has_xblocks = E->tabX.total() > 0;
   E->has_yblocks = E->tabY.total() > 0;
   auto upload_blocks = [&](const std::vector<PdcsBlock>& v, PdcsBlock** dst) -> int {
@@ -933,6 +1011,7 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   cudaFree(E->d_yred);
   cudaFree(E->d_gtp);
   free_table(E->tabX);
+  free_table(E->tabXs);
   free_table(E->tabY);
   cudaFree(E->d_unif_x);
   cudaFree(E->d_unif_y);
@@ -1422,14 +1501,70 @@ int pdcs_engine_set_comm(PdcsEngine* E, const unsigned char* h_id, int32_t rank,
   E->comm = comm;
   E->rank = rank;
   E->nranks = nranks;
-  if (!E->d_yred) CK(cudaMalloc(&E->d_yred, sizeof(double) * 8));
-  if (!E->d_gtp) CK(cudaMalloc(&E->d_gtp, sizeof(double) * std::max(E->n, 1)));
-  CK(cudaMemsetAsync(E->d_gtp, 0, sizeof(double) * std::max(E->n, 1), E->stream));
+  if (!E->d_yred) CK(cudaMalloc(&E->d_yred, sizeof(double) * 16));
+  // G^T y partials, padded for the equal-slice reduce-scatter (nranks * ceil(n / nranks))
+  const size_t gtp_len = (size_t)nranks * ((E->n + nranks - 1) / nranks) + 1;
+  if (E->d_gtp) cudaFree(E->d_gtp);
+  CK(cudaMalloc(&E->d_gtp, sizeof(double) * gtp_len));
+  CK(cudaMemsetAsync(E->d_gtp, 0, sizeof(double) * gtp_len, E->stream));
+  // until pdcs_engine_set_xsplit: every rank steps all of x-space
+  E->xs0 = 0;
+  E->xs1 = E->n;
+  E->xcnt = 0;
+  E->xcut.assign(nranks + 1, E->n);
+  E->xcut[0] = 0;
   CK(cudaStreamSynchronize(E->stream));
   // the captured graph (if any) predates the communicator
   if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }
   if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
   E->graph_slots = 0;
+  return 0;
+}
+
+int pdcs_engine_set_xsplit(PdcsEngine* E, const int32_t* h_cuts, int32_t nranks) {
+  if (!E || !h_cuts || !E->comm || nranks != E->nranks) {
+    g_err = "pdcs_engine_set_xsplit: needs the engine's communicator and its rank count";
+    return 2;
+  }
+  std::vector<int> cut(h_cuts, h_cuts + nranks + 1);
+  if (cut[0] != 0 || cut[nranks] != E->n) { g_err = "pdcs_engine_set_xsplit: cuts must span [0, n]"; return 2; }
+  for (int r = 0; r < nranks; ++r)
+    if (cut[r + 1] < cut[r]) { g_err = "pdcs_engine_set_xsplit: cuts must be nondecreasing"; return 2; }
+  for (const PdcsBlock& b : E->xblocks)
+    for (int r = 1; r < nranks; ++r)
+      if (cut[r] > b.start && cut[r] < b.start + b.dim) {
+        g_err = "pdcs_engine_set_xsplit: a cut splits a primal cone block";
+        return 2;
+      }
+  const int cnt = (E->n + nranks - 1) / nranks;
+  bool equal = true;
+  for (int r = 0; r <= nranks; ++r) equal = equal && cut[r] == std::min(r * cnt, E->n);
+  E->xcut = cut;
+  E->xcnt = equal ? cnt : 0;
+  E->xs0 = cut[E->rank];
+  E->xs1 = cut[E->rank + 1];
+  std::vector<PdcsBlock> mine;
+  for (const PdcsBlock& b : E->xblocks)
+    if (b.start >= E->xs0 && b.start < E->xs1) mine.push_back(b);
+  free_table(E->tabXs);
+  if (build_table(E->tabXs, mine, E->stream)) return 1;
+  E->xsplit = true;
+  // fewer reduction slots may be written now: the rest must read as zero
+  CK(cudaMemsetAsync(E->d_partX, 0, sizeof(double) * GX_N * E->capX, E->stream));
+  CK(cudaMemsetAsync(E->d_partT, 0, sizeof(double) * GT_N * E->capT, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }
+  if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
+  E->graph_slots = 0;
+  return 0;
+}
+
+int pdcs_allgather_x(PdcsEngine* E, double* const* d_vecs, int32_t count) {
+  if (!E || count < 0 || (count > 0 && !d_vecs)) { g_err = "pdcs_allgather_x: bad arguments"; return 2; }
+  if (!E->comm || !E->xsplit || E->nranks <= 1) return 0;
+  for (int i = 0; i < count; ++i)
+    if (nccl_x_allgather(E, d_vecs[i], E->stream)) return 1;
+  CK(cudaStreamSynchronize(E->stream));
   return 0;
 }
 

@@ -88,6 +88,9 @@ struct Engine {
   double* d_wpart_x = nullptr;  // partial sums of the G^T passes [n]
   BlockTable tabX, tabY;
   bool has_xblocks = false, has_yblocks = false;
+  std::vector<PdcsBlock> xblocks;  // primal cone blocks (host copy)
+  BlockTable tabXs;                // the blocks of this rank's x-slice (sharded)
+  bool xsplit = false;             // x-space split across the ranks (pdcs_engine_set_xsplit)
   // uniformity groups for preconditioning (blocks whose scale is made uniform)
   PdcsBlock* d_unif_x = nullptr;
   int n_unif_x = 0;
@@ -124,8 +127,12 @@ struct Engine {
   // sharded mode (row slice of G^ + NCCL communicator)
   void* comm = nullptr;       // ncclComm_t
   int rank = 0, nranks = 1;
-  double* d_yred = nullptr;   // all-reduced y-space line-search scalars [8]
-  double* d_gtp = nullptr;    // local G^T y_hat partial sums [n]
+  double* d_yred = nullptr;   // all-reduced trial scalars [16]: y sums, x sums, t sums
+  double* d_gtp = nullptr;    // local G^T y_hat partial sums [n, padded]
+  // x-space split: this rank steps x-slice [xs0, xs1) (all of x when not sharded)
+  int xs0 = 0, xs1 = 0;
+  int xcnt = 0;                // equal-slice length (0: slices cut at block boundaries)
+  std::vector<int> xcut;       // [nranks + 1]
 };
 
 }  // namespace pdcs

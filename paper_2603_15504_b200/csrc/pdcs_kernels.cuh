@@ -7,6 +7,7 @@ namespace pdcs {
 // All engine pointers, passed by value to kernels.
 struct KArgs {
   int n, m, nbox, m_zero, m_elem;
+  int x0, x1;  // x-space range this engine steps: [0, n), or the rank's slice when sharded
   const double *c, *h, *l, *u, *c0, *h0, *l0, *u0, *d1, *d2;
   double *x, *y, *xh, *yh, *xb, *yb, *xa, *ya;
   double *gx, *gty, *gxa, *gtya, *w, *gxh, *gth, *gtr, *xt;
@@ -30,7 +31,8 @@ struct CtrlFuse {
   const int* err;
 };
 __device__ void ctrl_ls_body(PdcsCtrl*, const double*, int, const double*, int, double*, const double*);
-__device__ void ctrl_beta_body(PdcsCtrl*, const double*, int, const double*, const int*);
+__device__ void ctrl_beta_body(PdcsCtrl*, const double*, int, const double*, const int*,
+                               const double*);
 __device__ __forceinline__ void fused_ctrl(const CtrlFuse& F);
 
 // gate: 0 = always run, 1 = skip when stopped, 2 = skip when stopped or the
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(BS, 5) k_step_x(KArgs A, double* part, int cap
   const bool inject = C->nan_after >= 0 && C->n_primal_proj >= C->nan_after;
   double acc[GX_N] = {0.0, 0.0, 0.0};
   const uint64_t ps = policy_stream(), pk = policy_keep_frac(A.keep_xt);
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x) {
+  for (int j = A.x0 + blockIdx.x * blockDim.x + threadIdx.x; j < A.x1; j += gridDim.x * blockDim.x) {
     double xn, gn;
     if (pend) {
       const double xo = ldc_hint<H>(A.x + j, ps);
@@ -935,7 +937,7 @@ __global__ void __launch_bounds__(BS) k_t_epilogue(KArgs A, double* part, int ca
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
   double acc[GT_N] = {0.0, 0.0, 0.0};
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x)
+  for (int j = A.x0 + blockIdx.x * blockDim.x + threadIdx.x; j < A.x1; j += gridDim.x * blockDim.x)
     t_epilogue<false>(A, j, A.gth[j], acc, 0);
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
 }
@@ -1128,11 +1130,13 @@ __device__ __forceinline__ void cta_sum_rows(const double* p, int cap, int n, do
 __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                              int capY, double* red, const double* yred) {
   double sx[GX_N], sy[GY_N];
-  cta_sum_rows<GX_N>(partX, capX, capX, sx);
-  if (yred) {
+  if (yred) {  // sharded: y sums then x sums, already all-reduced over the ranks
 #pragma unroll
     for (int q = 0; q < GY_N; ++q) sy[q] = yred[q];
+#pragma unroll
+    for (int q = 0; q < GX_N; ++q) sx[q] = yred[GY_N + q];
   } else {
+    cta_sum_rows<GX_N>(partX, capX, capX, sx);
     cta_sum_rows<GY_N>(partY, capY, capY, sy);
   }
   if (threadIdx.x != 0) return;
@@ -1203,9 +1207,14 @@ __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const doub
 // tests of an accepted iteration (engine.py:590-628, termination.py:150-160),
 // run by one whole CTA.
 __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const double* red,
-                               const int* err) {
+                               const int* err, const double* tred) {
   double st[GT_N];
-  cta_sum_rows<GT_N>(partT, capT, capT, st);
+  if (tred) {  // sharded: all-reduced over the ranks
+#pragma unroll
+    for (int q = 0; q < GT_N; ++q) st[q] = tred[q];
+  } else {
+    cta_sum_rows<GT_N>(partT, capT, capT, st);
+  }
   if (threadIdx.x != 0) return;
   const double rd2 = st[GT_RD2], ls = st[GT_LSUM], us = st[GT_USUM];
   if (*err) {  // numerical failure inside a projection (exp non-finite, rsoc bracket)
@@ -1261,9 +1270,9 @@ __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const
 }
 
 __global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
-                            const int* err) {
+                            const int* err, const double* tred) {
   if (C->stop || !C->accepted) return;
-  ctrl_beta_body(C, partT, capT, red, err);
+  ctrl_beta_body(C, partT, capT, red, err, tred);
 }
 
 // Controller folded into the last CTA of the kernel that writes the final
@@ -1283,7 +1292,7 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket) {
 __device__ __forceinline__ void fused_ctrl(const CtrlFuse& F) {
   if (!F.mode || !last_cta(F.ticket)) return;
   if (F.mode == 1) ctrl_ls_body(F.C, F.partA, F.capA, F.partB, F.capB, F.red, nullptr);
-  else ctrl_beta_body(F.C, F.partB, F.capB, F.red, F.err);
+  else ctrl_beta_body(F.C, F.partB, F.capB, F.red, F.err, nullptr);
   if (threadIdx.x == 0) *F.ticket = 0u;
 }
 

@@ -136,7 +136,11 @@ class DeviceEngine:
     use_preconditioner is off); mode "asis": the instance is used exactly as
     given, with its ConeSpec scales as the block scales (step-level API)."""
 
-    def __init__(self, work: ConicProblem, *, asis: bool = False, allow_nonuniform_dual_soc=False):
+    def __init__(self, work: ConicProblem, *, asis: bool = False, allow_nonuniform_dual_soc=False,
+                 x_pad: int = 0):
+        """x_pad: extra elements on the x-space iterate buffers (a sharded
+        engine's NCCL all-gather / reduce-scatter of x-slices needs
+        nranks * ceil(n / nranks) of them)."""
         lib = N.lib()
         torch = _torch()
         self.lib = lib
@@ -177,7 +181,7 @@ class DeviceEngine:
             names_y = ["y", "yh", "yb", "ya", "ypa", "gx", "gxa", "w", "gxh",
                        "ty0", "ty1", "ty2", "py0", "py1", "py2", "pgx"]
             for nm in names_x:
-                setattr(self, nm, f(n))
+                setattr(self, nm, f(n + x_pad))
             for nm in names_y:
                 setattr(self, nm, f(m))
         torch.cuda.synchronize()

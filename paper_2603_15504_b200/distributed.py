@@ -1,14 +1,21 @@
-"""Row-sharded multi-GPU solve.
+"""Sharded multi-GPU solve (with its recommended refinement).
 
 Rows of G^ (the y-space) are split into contiguous ranges, one per rank, cut
 only at cone-block boundaries (ZERO / NONNEG rows may be cut anywhere; SOC,
 EXP and DUAL_EXP blocks are indivisible) and balanced by nonzeros plus a row
-term.  Every rank keeps the whole x-space.  Per PDHG trial the device graph
-all-reduces (NCCL, in-graph) the five y-space line-search / beta sums and,
-for accepted trials, the n-vector of G_p^T y_hat_p partial sums; all x-space
-work is then identical on every rank.  The check path runs the reference's
-host logic on reductions that `ShardedDevice` combines across ranks with
-torch.distributed.
+term.  The x-space is split too: rank r steps x-slice [cut_r, cut_r+1)
+(equal slices when no primal cone block straddles them), keeping full-length
+buffers.  Per PDHG trial the device graph (NCCL, in-graph):
+  all-gathers x~ after the primal half-step (G_p x~ needs all of it),
+  all-reduces the 5 y-space + 3 x-space line-search sums,
+  reduce-scatters the G_p^T y_hat_p partial sums (each rank gets its slice),
+  all-reduces the 3 x-space beta sums.
+This moves the bytes of one all-reduce of G^T y per trial but splits the
+x-space streaming work (k_step_x and the G^T epilogue) N ways.  At a batch
+end the host flushes the pending Halpern step and all-gathers the x-space
+state, after which every rank holds identical full copies; the check path
+then runs the reference's host logic on reductions that `ShardedDevice`
+combines across ranks with torch.distributed.
 
 Preconditioning: every rank computes the Ruiz + Pock-Chambolle scaling of the
 FULL matrix on its GPU (exactly the single-GPU scaling), keeps its slice of D1
@@ -63,6 +70,41 @@ def partition_rows(problem: ConicProblem, world: int, row_weight: float = 1.0):
         bounds.append(int(best))
     bounds.append(m)
     return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+def allowed_xcuts(problem: ConicProblem) -> np.ndarray:
+    """x-space indices at which the x-space may be cut: anywhere inside the
+    box coordinates, then only primal cone-block boundaries."""
+    cuts = list(range(0, problem.num_box + 1))
+    pos = problem.num_box
+    for spec in problem.primal_cones:
+        pos += spec.dim
+        cuts.append(pos)
+    return np.unique(np.asarray(cuts + [problem.n], dtype=np.int64))
+
+
+def partition_cols(problem: ConicProblem, world: int) -> list[int]:
+    """x-slice cuts [0 = c_0 <= ... <= c_world = n]: the equal split
+    c_r = min(r ceil(n / world), n) when it cuts no primal cone block (the
+    engine then uses NCCL all-gather / reduce-scatter), else the allowed cut
+    nearest to r n / world."""
+    n = problem.n
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    cnt = -(-n // world) if n else 0
+    equal = [min(r * cnt, n) for r in range(world + 1)]
+    allowed = allowed_xcuts(problem)
+    ok = set(allowed.tolist())
+    if all(c in ok for c in equal):
+        return equal
+    cuts = [0]
+    for r in range(1, world):
+        target = n * r / world
+        i = int(np.searchsorted(allowed, target))
+        cand = [int(allowed[j]) for j in (i - 1, i) if 0 <= j < len(allowed)]
+        cuts.append(max(min(cand, key=lambda c: abs(c - target)), cuts[-1]))
+    cuts.append(n)
+    return cuts
 
 
 def slice_problem(work: ConicProblem, r0: int, r1: int) -> ConicProblem:
@@ -142,6 +184,19 @@ class ShardedDevice:
     def __getattr__(self, name):
         return getattr(self._dev, name)
 
+    # x-space state the device loop leaves stale outside each rank's slice
+    X_STATE = ("x", "xh", "xb", "gty", "gth")
+
+    def flush(self):
+        """Apply the pending Halpern step, then give every rank full copies of
+        the x-space state (each rank only stepped its x-slice)."""
+        import ctypes
+
+        self._dev.flush()
+        bufs = [getattr(self._dev, nm) for nm in self.X_STATE]
+        arr = (ctypes.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs])
+        N.check(self._dev.lib.pdcs_allgather_x(self._dev.handle, arr, len(bufs)), "pdcs_allgather_x")
+
     def spmv(self, transpose: bool, src, dst):
         self._dev.spmv(transpose, src, dst)
         if transpose:
@@ -193,13 +248,15 @@ def _make_sharded_loop_class():
 
             work = self.work
             enabled = 1 if (options.use_preconditioner and work.G.nnz > 0) else 0
-            full = DeviceEngine(work, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc)
+            full = DeviceEngine(work, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc,
+                                x_pad=self._world)
             full.precondition(enabled, options.ruiz_iterations, options.use_pock_chambolle)
             stats = full.stats()
             r0, r1 = partition_rows(work, self._world)[self._rank]
             self.row_range = (r0, r1)
             local = slice_problem(work, r0, r1)
-            dev = DeviceEngine(local, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc)
+            dev = DeviceEngine(local, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc,
+                               x_pad=self._world)
             with torch.cuda.stream(dev.stream):
                 if r1 > r0:
                     dev.d1[: r1 - r0].copy_(full.d1[r0:r1])
@@ -219,6 +276,11 @@ def _make_sharded_loop_class():
             dist.broadcast_object_list(buf, src=0, group=self._group)
             N.check(dev.lib.pdcs_engine_set_comm(dev.handle, buf[0], self._rank, self._world),
                     "pdcs_engine_set_comm")
+            import ctypes
+
+            self.xcuts = partition_cols(work, self._world)
+            cuts = (ctypes.c_int32 * len(self.xcuts))(*self.xcuts)
+            N.check(dev.lib.pdcs_engine_set_xsplit(dev.handle, cuts, self._world), "pdcs_engine_set_xsplit")
             ar = torch_allreduce(self._group)
 
             def vec_ar(t):

@@ -14,7 +14,8 @@ from dist_emulation import sharded_run
 from oracle import pdcs_oracle as O
 from paper_2603_15504_b200 import instances
 from paper_2603_15504_b200.distributed import (
-    GAP_Y_SUM, MET_Y_MAX, MET_Y_SUM, allowed_cuts, combine, partition_rows, slice_problem)
+    GAP_Y_SUM, MET_Y_MAX, MET_Y_SUM, allowed_cuts, allowed_xcuts, combine, partition_cols,
+    partition_rows, slice_problem)
 from paper_2603_15504_b200.model import Cone, rsoc_to_soc
 
 
@@ -26,7 +27,14 @@ def _free_port():
     return port
 
 
+def _prim():
+    from golden_io import load, problem
+
+    return problem(load("solve_prim"))
+
+
 PROBLEMS = {
+    "prim": _prim,
     "lp": functools.partial(instances.lp_large, m=600, n=1200, nnz_per_row=5, eq_frac=0.3, seed=5),
     "socp": functools.partial(instances.group_robust_regression, ngroups=30, gsize=5, q=80,
                               nnz_per_row=10, seed=2),
@@ -50,6 +58,19 @@ def test_partition_cuts_only_at_block_boundaries(name, world):
     if name == "lp":  # elementwise rows: nnz balanced within a few rows
         nnz = [work.G._csr[r0:r1].nnz for r0, r1 in parts]
         assert max(nnz) - min(nnz) <= 20
+
+
+@pytest.mark.parametrize("name", sorted(PROBLEMS))
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_xsplit_cuts_only_at_primal_block_boundaries(name, world):
+    work = rsoc_to_soc(PROBLEMS[name]())
+    cuts = partition_cols(work, world)
+    assert len(cuts) == world + 1 and cuts[0] == 0 and cuts[-1] == work.n
+    assert all(a <= b for a, b in zip(cuts, cuts[1:]))
+    assert set(cuts) <= set(allowed_xcuts(work).tolist())
+    if not work.primal_cones:  # equal slices: the engine's all-gather / reduce-scatter path
+        cnt = -(-work.n // world)
+        assert cuts == [min(r * cnt, work.n) for r in range(world + 1)]
 
 
 def test_slices_reassemble_the_matrix():
@@ -89,7 +110,7 @@ def test_combine_plan():
     assert GAP_Y_SUM == (1, 3)
 
 
-@pytest.mark.parametrize("name,world", [("lp", 2), ("socp", 2), ("exp", 3), ("rsoc", 2)])
+@pytest.mark.parametrize("name,world", [("lp", 2), ("socp", 2), ("exp", 3), ("rsoc", 2), ("prim", 3)])
 def test_sharded_iterations_match_single_process_oracle(tmp_path, name, world):
     iters = 40
     out = str(tmp_path / "sharded.npz")

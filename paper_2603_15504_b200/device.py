@@ -47,6 +47,97 @@ def _empty_f64(n):
     return torch.zeros(max(int(n), 1), dtype=torch.float64, device="cuda")
 
 
+def _slab(dtype, sizes: dict, align: int = 64) -> dict:
+    """Zeroed device views carved out of ONE allocation: a fresh cudaMalloc per
+    large buffer costs ~14 ms on the B200 box (tools/xfer_probe.py: 33
+    vectors 0.47 s, one 4 GB slab 5 ms), which dominated engine setup."""
+    torch = _torch()
+    offs, total = {}, 0
+    for name, count in sizes.items():
+        offs[name] = total
+        total += -(-max(int(count), 1) // align) * align
+    buf = torch.zeros(max(total, 1), dtype=dtype, device="cuda")
+    return {name: buf[off:off + max(int(sizes[name]), 1)] for name, off in offs.items()}
+
+
+_STAGE_BYTES = 32 << 20
+_stage_bufs = None
+
+
+def _stages():
+    """Two reusable pinned host buffers for double-buffered transfers."""
+    global _stage_bufs
+    if _stage_bufs is None:
+        torch = _torch()
+        _stage_bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+    return _stage_bufs
+
+
+def h2d(dst, arr, stream) -> None:
+    """Host array -> device view `dst` (same dtype) through double-buffered
+    pinned staging on `stream` (~30 GB/s; a pageable copy runs at ~10)."""
+    torch = _torch()
+    np_dtype = {torch.float64: np.float64, torch.int32: np.int32}[dst.dtype]
+    a = np.ascontiguousarray(arr, dtype=np_dtype).reshape(-1)
+    if a.size == 0:
+        return
+    if a.nbytes < (1 << 20):
+        with torch.cuda.stream(stream):
+            dst[: a.size].copy_(torch.from_numpy(a), non_blocking=False)
+        stream.synchronize()
+        return
+    src = a.view(np.uint8)
+    dbytes = dst[: a.size].view(torch.uint8)
+    st = _stages()
+    done = [None, None]
+    with torch.cuda.stream(stream):
+        for i, off in enumerate(range(0, src.size, _STAGE_BYTES)):
+            b = i & 1
+            if done[b] is not None:
+                done[b].synchronize()
+            k = min(_STAGE_BYTES, src.size - off)
+            st[b][:k].numpy()[:] = src[off:off + k]
+            dbytes[off:off + k].copy_(st[b][:k], non_blocking=True)
+            done[b] = torch.cuda.Event()
+            done[b].record(stream)
+    stream.synchronize()
+
+
+def d2h(src, n: int, stream) -> np.ndarray:
+    """First n elements of a device tensor -> new host array, through the
+    pinned staging buffers (the next chunk's DMA overlaps this chunk's copy)."""
+    torch = _torch()
+    np_dtype = {torch.float64: np.float64, torch.int32: np.int32}[src.dtype]
+    out = np.empty(n, dtype=np_dtype)
+    if n == 0:
+        return out
+    if out.nbytes < (1 << 20):
+        stream.synchronize()
+        return src[:n].cpu().numpy().copy()
+    ob = out.view(np.uint8)
+    sb = src[:n].view(torch.uint8)
+    st = _stages()
+    chunks = list(range(0, ob.size, _STAGE_BYTES))
+    events = []
+    with torch.cuda.stream(stream):
+        def issue(i):
+            off = chunks[i]
+            k = min(_STAGE_BYTES, ob.size - off)
+            st[i & 1][:k].copy_(sb[off:off + k], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            events.append(ev)
+
+        issue(0)
+        for i, off in enumerate(chunks):
+            if i + 1 < len(chunks):
+                issue(i + 1)
+            events[i].synchronize()
+            k = min(_STAGE_BYTES, ob.size - off)
+            ob[off:off + k] = st[i & 1][:k].numpy()
+    return out
+
+
 class DeviceCSR:
     """Device copy of a CSR matrix and of its (device-built) transpose, for
     SparseMatrix.matvec / rmatvec."""
@@ -151,39 +242,36 @@ class DeviceEngine:
         csr = work.G._csr
         self.nnz = int(csr.nnz)
         self.m_zero, self.m_elem = dual_layout(work)
+        nb, nnz = work.num_box, self.nnz
+        names_x = ["x", "xh", "xb", "xa", "xpa", "gty", "gtya", "gth", "gtr", "xt",
+                   "tx0", "tx1", "tx2", "px0", "px1", "px2", "pgty"]
+        names_y = ["y", "yh", "yb", "ya", "ypa", "gx", "gxa", "w", "gxh",
+                   "ty0", "ty1", "ty2", "py0", "py1", "py2", "pgx"]
+        f64 = {"g_val0": nnz, "g_val": nnz, "gt_val": nnz, "c0": n, "h0": m, "l0": nb, "u0": nb,
+               "c": n, "h": m, "l": nb, "u": nb, "d1": m, "d2": n}
+        f64.update({nm: n + x_pad for nm in names_x})
+        f64.update({nm: m for nm in names_y})
+        i32 = {"g_rowptr": m + 1, "g_colidx": nnz, "gt_rowptr": n + 1, "gt_colidx": nnz, "perm": nnz}
         with torch.cuda.stream(self.stream):
-            f = _empty_f64
-            self.g_rowptr = _dev_i32(csr.indptr)
-            self.g_colidx = _dev_i32(csr.indices)
-            self.g_val0 = _dev_f64(csr.data)
-            self.g_val = f(self.nnz)
-            self.gt_rowptr = torch.zeros(n + 1, dtype=torch.int32, device="cuda")
-            self.gt_colidx = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
-            self.gt_val = f(self.nnz)
-            self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
-            self.c0 = _dev_f64(work.c)
-            self.h0 = _dev_f64(work.h)
-            self.l0 = _dev_f64(work.l)
-            self.u0 = _dev_f64(work.u)
-            self.c, self.h, self.l, self.u = f(n), f(m), f(work.num_box), f(work.num_box)
-            if asis:
-                d2 = np.ones(n)
-                for spec, sl in _slices(work.primal_cones, work.num_box):
-                    d2[sl] = spec.scale
-                d1 = np.ones(m)
-                for spec, sl in _slices(work.dual_cones, 0):
-                    d1[sl] = spec.scale
-                self.d1, self.d2 = _dev_f64(d1), _dev_f64(d2)
-            else:
-                self.d1, self.d2 = f(m), f(n)
-            names_x = ["x", "xh", "xb", "xa", "xpa", "gty", "gtya", "gth", "gtr", "xt",
-                       "tx0", "tx1", "tx2", "px0", "px1", "px2", "pgty"]
-            names_y = ["y", "yh", "yb", "ya", "ypa", "gx", "gxa", "w", "gxh",
-                       "ty0", "ty1", "ty2", "py0", "py1", "py2", "pgx"]
-            for nm in names_x:
-                setattr(self, nm, f(n + x_pad))
-            for nm in names_y:
-                setattr(self, nm, f(m))
+            for name, view in {**_slab(torch.float64, f64), **_slab(torch.int32, i32)}.items():
+                setattr(self, name, view)
+        torch.cuda.synchronize()
+        h2d(self.g_rowptr, csr.indptr, self.stream)
+        h2d(self.g_colidx, csr.indices, self.stream)
+        h2d(self.g_val0, csr.data, self.stream)
+        h2d(self.c0, work.c, self.stream)
+        h2d(self.h0, work.h, self.stream)
+        h2d(self.l0, work.l, self.stream)
+        h2d(self.u0, work.u, self.stream)
+        if asis:
+            d2 = np.ones(n)
+            for spec, sl in _slices(work.primal_cones, work.num_box):
+                d2[sl] = spec.scale
+            d1 = np.ones(m)
+            for spec, sl in _slices(work.dual_cones, 0):
+                d1[sl] = spec.scale
+            h2d(self.d1, d1, self.stream)
+            h2d(self.d2, d2, self.stream)
         torch.cuda.synchronize()
 
         pk = [KIND_CODE[s.kind] for s in work.primal_cones]
@@ -355,16 +443,10 @@ class DeviceEngine:
                 b.zero_()
 
     def upload(self, dst, arr):
-        torch = _torch()
-        a = np.ascontiguousarray(arr, dtype=np.float64)
-        with torch.cuda.stream(self.stream):
-            if a.size:
-                dst[: a.size].copy_(torch.from_numpy(a))
-        self.stream.synchronize()
+        h2d(dst, arr, self.stream)
 
     def host(self, t, n) -> np.ndarray:
-        self.stream.synchronize()
-        return t[:n].cpu().numpy().copy() if n else np.zeros(0)
+        return d2h(t, n, self.stream)
 
     def xh_host(self, name):
         return self.host(getattr(self, name), self.n)

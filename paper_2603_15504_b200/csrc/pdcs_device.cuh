@@ -169,6 +169,30 @@ struct WarpGrp {
   __device__ void sync() const { __syncwarp(); }
 };
 
+// W lanes of a warp per block (32 / W blocks side by side).  Every collective
+// names only the group's lanes, so the groups of one warp may diverge
+// (different branches or trip counts) without waiting on each other.
+template <int W>
+struct SubGrp {
+  int rank, size;
+  unsigned mask;
+  __device__ SubGrp()
+      : rank(threadIdx.x & (W - 1)), size(W),
+        mask((W == 32 ? 0xffffffffu : ((1u << W) - 1u)) << ((threadIdx.x & 31) & ~(W - 1))) {}
+  __device__ double sum(double v) const {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) v += __shfl_down_sync(mask, v, off, W);
+    return __shfl_sync(mask, v, 0, W);
+  }
+  __device__ double max(double v) const {
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) v = nanmax(v, __shfl_down_sync(mask, v, off, W));
+    return __shfl_sync(mask, v, 0, W);
+  }
+  __device__ int all(int v) const { return (__ballot_sync(mask, v) & mask) == mask; }
+  __device__ void sync() const { __syncwarp(mask); }
+};
+
 struct CtaGrp {
   int rank, size;
   double* sh;  // >= 33 doubles of shared scratch

@@ -298,27 +298,31 @@ int launch_rowred(const SpmvPlan& P, const double* val, double* out, cudaStream_
 
 // ---- cone block tables -------------------------------------------------------
 int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bool giant_ok = false) {
-  std::vector<PdcsBlock> ex, th, wa, ct, gi;
+  std::vector<PdcsBlock> ex, th, hf, wa, ct, gi;
   for (auto& b : blocks) {
     if ((b.kind == PDCS_EXP || b.kind == PDCS_DUAL_EXP) && b.dim == 3) ex.push_back(b);
     else if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
+    else if (b.dim <= HALF_CLASS_MAX) hf.push_back(b);
     else if (b.dim <= WARP_CLASS_MAX) wa.push_back(b);
     else if (giant_ok && b.kind == PDCS_SOC && b.dim > GIANT_MIN) gi.push_back(b);
     else ct.push_back(b);
   }
   T.n_exp = (int)ex.size();
   T.n_thread = (int)th.size();
+  T.n_half = (int)hf.size();
   T.n_warp = (int)wa.size();
   T.n_cta = (int)ct.size();
   T.n_giant = (int)gi.size();
   std::vector<PdcsBlock> all;
   all.insert(all.end(), ex.begin(), ex.end());
   all.insert(all.end(), th.begin(), th.end());
+  all.insert(all.end(), hf.begin(), hf.end());
   all.insert(all.end(), wa.begin(), wa.end());
   all.insert(all.end(), ct.begin(), ct.end());
   all.insert(all.end(), gi.begin(), gi.end());
   T.g_exp = T.n_exp ? grid_for(T.n_exp) : 0;
   T.g_thread = T.n_thread ? grid_for(T.n_thread) : 0;
+  T.g_half = T.n_half ? grid_for(T.n_half, BS / 16) : 0;
   T.g_warp = T.n_warp ? grid_for(T.n_warp, BS / 32) : 0;
   T.g_cta = T.n_cta ? std::min(T.n_cta, MAX_GRID) : 0;
   T.g_giant = T.n_giant ? GIANT_GRID : 0;
@@ -358,6 +362,12 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
   }
   slot += T.g_thread;
   base += T.n_thread;
+  if (T.n_half) {
+    k_blk_half<OP><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
+    CKL();
+  }
+  slot += T.g_half;
+  base += T.n_half;
   if (T.n_warp) {
     k_blk_warp<OP><<<T.g_warp, BS, 0, s>>>(base, T.n_warp, A, P, part, cap, slot, gate);
     CKL();

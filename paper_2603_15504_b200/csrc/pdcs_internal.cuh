@@ -52,13 +52,13 @@ struct PanelPlan {
 
 // Cone-block table of one space split into size classes.
 struct BlockTable {
-  PdcsBlock* d_all = nullptr;  // exp class, thread class, warp class, cta class, giant class
-  int n_exp = 0, n_thread = 0, n_warp = 0, n_cta = 0, n_giant = 0;
-  int g_exp = 0, g_thread = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
+  PdcsBlock* d_all = nullptr;  // exp, thread, half-warp, warp, cta, giant classes in that order
+  int n_exp = 0, n_thread = 0, n_half = 0, n_warp = 0, n_cta = 0, n_giant = 0;
+  int g_exp = 0, g_thread = 0, g_half = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
   double* d_gpart = nullptr;  // giant-block partial sums [n_giant][2][g_giant]
   double* d_gcoef = nullptr;  // giant-block SOC coefficients [n_giant][8]
-  int total() const { return n_exp + n_thread + n_warp + n_cta + n_giant; }
-  int grids() const { return g_exp + g_thread + g_warp + g_cta + g_giant; }
+  int total() const { return n_exp + n_thread + n_half + n_warp + n_cta + n_giant; }
+  int grids() const { return g_exp + g_thread + g_half + g_warp + g_cta + g_giant; }
 };
 
 constexpr int GIANT_MIN = 1 << 16;  // uniform dual SOC blocks above this use the whole grid
@@ -68,6 +68,7 @@ constexpr int TILE_ROWS = BS;    // rows per CSR-stream tile (one per thread in 
 constexpr int TILE_NNZ = 2048;   // entries per tile; longer rows use the chunked path
 constexpr int WARP_CLASS_MAX = 4096;  // dims above this get a whole CTA
 constexpr int THREAD_CLASS_MAX = 4;   // dims up to this get one thread
+constexpr int HALF_CLASS_MAX = 16;    // then up to this 16 lanes (two blocks per warp)
 constexpr int CTA_BLOCK_THREADS = 512;
 
 // Reduction groups of one line-search trial.

@@ -550,6 +550,25 @@ __global__ void __launch_bounds__(BS) k_blk_thread(const PdcsBlock* tab, int nb,
   if (OP != OP_PROJECT) block_store_mask<NQ>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }
 
+// Small blocks (THREAD_CLASS_MAX < dim <= HALF_CLASS_MAX): 16 lanes per
+// block, two blocks per warp.
+template <int OP>
+__global__ void __launch_bounds__(BS) k_blk_half(const PdcsBlock* tab, int nb, KArgs A,
+                                                 BlkParams P, double* part, int cap, int slot0,
+                                                 int gate) {
+  if (gated(A.ctrl, gate)) return;
+  constexpr int NQ = OpNQ<OP>::v;
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+  SubGrp<16> g;
+  const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
+  const int gn = (gridDim.x * blockDim.x) >> 4;
+  for (int i = gi; i < nb; i += gn) do_block<SubGrp<16>, OP>(g, tab[i], A, P, acc);
+  __syncwarp();
+  if (OP != OP_PROJECT) block_store_mask<NQ>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
 template <int OP>
 __global__ void __launch_bounds__(BS) k_blk_warp(const PdcsBlock* tab, int nb, KArgs A,
                                                  BlkParams P, double* part, int cap, int slot0,

@@ -315,9 +315,12 @@ __device__ inline void exp_bracket(double r, double s, double t, double pdist, d
   hi_out = hi;
 }
 
-__device__ inline double exp_root(double r, double s, double t, double lo, double hi) {
+// x0: optional Newton start (the block's root from the previous PDHG trial);
+// NaN or outside (lo, hi) means the reference's midpoint start.
+__device__ inline double exp_root(double r, double s, double t, double lo, double hi,
+                                  double x0 = NAN) {
   const int newton = 20, total = 100;
-  double x = 0.5 * (lo + hi);
+  double x = (x0 > lo && x0 < hi) ? x0 : 0.5 * (lo + hi);
   bool done = false;
   for (int i = 0; i < newton; ++i) {
     double f, df;
@@ -370,7 +373,11 @@ __device__ inline bool exp_from_rho(double r, double s, double t, double rho, do
 
 // Euclidean projection of (r, s, t) onto K_exp (cones.py:298-326).  Sets *err
 // for non-finite input (the reference raises NumericalError).
-__device__ inline void proj_exp3(double r, double s, double t, double* o, int* err) {
+// rho_io (optional): warm start for the Newton root-find, updated with the
+// root found -- consecutive PDHG trials project nearby points, so Newton
+// starts next to its root instead of at the bracket midpoint.
+__device__ inline void proj_exp3(double r, double s, double t, double* o, int* err,
+                                 double* rho_io = nullptr) {
   if (!(isfinite(r) && isfinite(s) && isfinite(t))) {
     *err = PDCS_ERR_EXP_NONFINITE;
     o[0] = r; o[1] = s; o[2] = t;
@@ -408,7 +415,8 @@ __device__ inline void proj_exp3(double r, double s, double t, double* o, int* e
   }
   double lo, hi;
   exp_bracket(r, s, t, pdist, ddist, lo, hi);
-  double rho = exp_root(r, s, t, lo, hi);
+  double rho = exp_root(r, s, t, lo, hi, rho_io ? *rho_io : NAN);
+  if (rho_io) *rho_io = rho;
   double pr[3], dr;
   if (exp_from_rho(r, s, t, rho, pr, &dr) && dr <= pdist) {
     o[0] = pr[0]; o[1] = pr[1]; o[2] = pr[2];
@@ -418,9 +426,10 @@ __device__ inline void proj_exp3(double r, double s, double t, double* o, int* e
 }
 
 // Dual cone via Moreau: P_{K*}(v) = v + P_K(-v) (cones.py:329-331).
-__device__ inline void proj_dual_exp3(double r, double s, double t, double* o, int* err) {
+__device__ inline void proj_dual_exp3(double r, double s, double t, double* o, int* err,
+                                      double* rho_io = nullptr) {
   double q[3];
-  proj_exp3(-r, -s, -t, q, err);
+  proj_exp3(-r, -s, -t, q, err, rho_io);
   o[0] = r + q[0]; o[1] = s + q[1]; o[2] = t + q[2];
 }
 

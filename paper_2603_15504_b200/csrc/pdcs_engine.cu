@@ -174,6 +174,7 @@ KArgs make_args(const Engine* E) {
   A.err = E->d_err;
   A.keep_xt = E->keep_xt;
   A.keep_yh = E->keep_yh;
+  A.exp_rho = E->d_exp_rho;
   return A;
 }
 
@@ -874,6 +875,14 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc)) return fail(1);
   E->xblocks = xb;
   E->has_xblocks = E->tabX.total() > 0;
+  if (E->tabY.n_exp) {  // Newton warm starts of the dual exp blocks, NaN = cold
+    const size_t cnt = 2 * (size_t)E->tabY.n_exp;
+    if (cudaMalloc(&E->d_exp_rho, sizeof(double) * cnt) != cudaSuccess) return fail(1);
+    std::vector<double> nan_init(cnt, NAN);
+    if (cudaMemcpy(E->d_exp_rho, nan_init.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice) !=
+        cudaSuccess)
+      return fail(1);
+  }
   E->has_yblocks = E->tabY.total() > 0;
   auto upload_blocks = [&](const std::vector<PdcsBlock>& v, PdcsBlock** dst) -> int {
     if (v.empty()) return 0;
@@ -1022,6 +1031,7 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   cudaFree(E->d_gtp);
   free_table(E->tabX);
   free_table(E->tabXs);
+  cudaFree(E->d_exp_rho);
   free_table(E->tabY);
   cudaFree(E->d_unif_x);
   cudaFree(E->d_unif_y);

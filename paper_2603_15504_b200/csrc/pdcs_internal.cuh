@@ -91,6 +91,7 @@ struct Engine {
   bool has_xblocks = false, has_yblocks = false;
   std::vector<PdcsBlock> xblocks;  // primal cone blocks (host copy)
   BlockTable tabXs;                // the blocks of this rank's x-slice (sharded)
+  double* d_exp_rho = nullptr;     // Newton warm starts of the dual exp blocks [2 n_exp]
   bool xsplit = false;             // x-space split across the ranks (pdcs_engine_set_xsplit)
   // uniformity groups for preconditioning (blocks whose scale is made uniform)
   PdcsBlock* d_unif_x = nullptr;

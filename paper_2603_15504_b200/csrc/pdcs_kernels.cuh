@@ -15,6 +15,7 @@ struct KArgs {
   PdcsCtrl* ctrl;
   int* err;
   float keep_xt, keep_yh;  // evict_last fractions of the gathered x~ / y_hat lines
+  double* exp_rho;         // per dual exp block: Newton warm starts of its 2 projections (or null)
 };
 
 // Controller folded into a step kernel (mode 0 off, 1 line search after the
@@ -469,9 +470,10 @@ __device__ __forceinline__ void do_block(const Grp& g, const PdcsBlock& b, const
 
 // Exponential-cone blocks (always 3-dimensional, block-uniform scale): one
 // thread per block with straight-line code, no generic segment machinery.
-__device__ __forceinline__ void exp_or_dual(int kind, const double* v, double* o, int* err) {
-  if (kind == PDCS_EXP) proj_exp3(v[0], v[1], v[2], o, err);
-  else proj_dual_exp3(v[0], v[1], v[2], o, err);
+__device__ __forceinline__ void exp_or_dual(int kind, const double* v, double* o, int* err,
+                                            double* rho = nullptr) {
+  if (kind == PDCS_EXP) proj_exp3(v[0], v[1], v[2], o, err, rho);
+  else proj_dual_exp3(v[0], v[1], v[2], o, err, rho);
 }
 
 template <int OP>
@@ -506,10 +508,11 @@ __global__ void __launch_bounds__(BS, 4) k_blk_exp(const PdcsBlock* tab, int nb,
       }
     } else if (OP == OP_STEP_Y) {
       for (int q = 0; q < 3; ++q) v[q] = A.yh[s + q];
-      exp_or_dual(dual_kind(b.kind), v, o, &err);
+      double* rho = A.exp_rho ? A.exp_rho + 2 * (size_t)i : nullptr;  // warm starts
+      exp_or_dual(dual_kind(b.kind), v, o, &err, rho);
       double res[3], rp[3];
       for (int q = 0; q < 3; ++q) res[q] = A.gxh[s + q] - A.h[s + q];
-      exp_or_dual(b.kind, res, rp, &err);
+      exp_or_dual(b.kind, res, rp, &err, rho ? rho + 1 : nullptr);
       for (int q = 0; q < 3; ++q) {
         const int r = s + q;
         const double yn = A.y[r], p = o[q], hi = A.h[r];

@@ -691,10 +691,14 @@ int launch_slot(Engine* E) {
   if (xblk && launch_blocks<OP_TLAM>(TX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s)) return 1;
   if (xblk) mark(s, "blocks_t");
   const double* tred = nullptr;
-  if (E->comm) {  // sharded: the three x-space beta sums over all ranks
+  if (E->comm) {
+    // sharded: the three x-space beta sums over all ranks, plus the ranks'
+    // projection error codes, so every rank takes the same stop decision
     k_finalize<<<1, BS, 0, s>>>(E->d_partT, E->capT, E->capT, GT_N, 0u, E->d_yred + 8);
     CKL();
-    if (nccl_allreduce(E->d_yred + 8, E->d_yred + 8, GT_N, E->comm, s)) return 1;
+    k_err_to_double<<<1, 1, 0, s>>>(E->d_err, E->d_yred + 8 + GT_N);
+    CKL();
+    if (nccl_allreduce(E->d_yred + 8, E->d_yred + 8, GT_N + 1, E->comm, s)) return 1;
     mark(s, "allreduce_t");
     tred = E->d_yred + 8;
   }

@@ -1239,8 +1239,11 @@ __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const
   }
   if (threadIdx.x != 0) return;
   const double rd2 = st[GT_RD2], ls = st[GT_LSUM], us = st[GT_USUM];
-  if (*err) {  // numerical failure inside a projection (exp non-finite, rsoc bracket)
-    C->error = *err;
+  int e = *err;
+  if (tred && e == 0 && tred[GT_N] > 0.0)  // another rank's projection failed
+    e = (int)dmin(tred[GT_N], (double)PDCS_ERR_BETA);
+  if (e) {  // numerical failure inside a projection (exp non-finite, rsoc bracket)
+    C->error = e;
     C->stop = 1;
     C->reason = PDCS_STOP_ERROR;
     C->accepted = 0;
@@ -1290,6 +1293,9 @@ __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const
   else if (kb >= C->k_bar_stop) { C->stop = 1; C->reason = PDCS_STOP_BATCH; }
   else if (C->print_freq > 0 && kb % C->print_freq == 0) { C->stop = 1; C->reason = PDCS_STOP_PRINT; }
 }
+
+// sharded mode: the rank's projection error code as a double for the all-reduce
+__global__ void k_err_to_double(const int* err, double* out) { *out = (double)*err; }
 
 __global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
                             const int* err, const double* tred) {

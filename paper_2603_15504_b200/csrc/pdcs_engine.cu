@@ -208,7 +208,12 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   CK(cudaMalloc(&P.d_tiles, sizeof(int) * tiles.size()));
   CK(cudaMemcpyAsync(P.d_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
-  const int chunk = 8192;
+  // entries per long-row chunk (one CTA reduction each); PDCS_TUNE=chunk=N overrides
+  int chunk = 8192;
+  if (const char* env = getenv("PDCS_TUNE")) {
+    const char* p = strstr(env, "chunk=");
+    if (p && (p == env || p[-1] == ',')) chunk = std::max(256, atoi(p + 6));
+  }
   std::vector<int> lrows, lfirst;
   std::vector<int4> chunks;
   for (int r = 0; r < nrows; ++r) {

@@ -612,12 +612,19 @@ __global__ void __launch_bounds__(CTA_BLOCK_THREADS) k_blk_cta(const PdcsBlock* 
 // reductions ||x||^2, ||x_hat - x||^2, c.x_hat (engine.py:155-161, 207-218,
 // 246-277, 602-610).  Cone coordinates are left unprojected for k_blk_*.
 template <bool H>
-__global__ void __launch_bounds__(BS, 5) k_step_x(KArgs A, double* part, int cap) {
+__global__ void __launch_bounds__(BS, 8) k_step_x(KArgs A, double* part, int cap) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
+  // the Halpern / step coefficients live in shared memory (register pressure)
+  __shared__ double kc[8];
+  if (threadIdx.x == 0) {
+    kc[0] = C->pa; kc[1] = C->pb; kc[2] = C->pbeta; kc[3] = C->peta; kc[4] = C->pW; kc[5] = C->tau;
+    kc[6] = 1.0 + C->pbeta; kc[7] = C->pW + C->peta;
+  }
+  __syncthreads();
+  const double &a = kc[0], &b = kc[1], &be = kc[2], &et = kc[3], &W = kc[4], &tau = kc[5];
+  const double &opb = kc[6], &tot = kc[7];
   const bool pend = C->pending != 0;
-  const double a = C->pa, b = C->pb, be = C->pbeta, et = C->peta, W = C->pW, tau = C->tau;
-  const double opb = 1.0 + be, tot = W + et;
   const bool inject = C->nan_after >= 0 && C->n_primal_proj >= C->nan_after;
   double acc[GX_N] = {0.0, 0.0, 0.0};
   const uint64_t ps = policy_stream(), pk = policy_keep_frac(A.keep_xt);

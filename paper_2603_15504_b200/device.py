@@ -112,8 +112,9 @@ def d2h(src, n: int, stream) -> np.ndarray:
     if n == 0:
         return out
     if out.nbytes < (1 << 20):
-        stream.synchronize()
-        return src[:n].cpu().numpy().copy()
+        with torch.cuda.stream(stream):
+            host = src[:n].cpu()
+        return host.numpy().copy()
     ob = out.view(np.uint8)
     sb = src[:n].view(torch.uint8)
     st = _stages()
@@ -154,7 +155,7 @@ class DeviceCSR:
         self.tci = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
         self.tva = torch.empty(max(self.nnz, 1), dtype=torch.float64, device="cuda")
         self.perm = torch.empty(max(self.nnz, 1), dtype=torch.int32, device="cuda")
-        torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
         N.check(lib.pdcs_transpose_csr(self.m, self.n, self.nnz, _ptr(self.rp), _ptr(self.ci),
                                        _ptr(self.va), _ptr(self.trp), _ptr(self.tci),
                                        _ptr(self.tva), _ptr(self.perm), None), "pdcs_transpose_csr")
@@ -255,7 +256,9 @@ class DeviceEngine:
         with torch.cuda.stream(self.stream):
             for name, view in {**_slab(torch.float64, f64), **_slab(torch.int32, i32)}.items():
                 setattr(self, name, view)
-        torch.cuda.synchronize()
+        # stream-level syncs only: a device-wide sync is illegal while another
+        # thread's engine captures its graph (concurrent solves, batch.py)
+        self.stream.synchronize()
         h2d(self.g_rowptr, csr.indptr, self.stream)
         h2d(self.g_colidx, csr.indices, self.stream)
         h2d(self.g_val0, csr.data, self.stream)
@@ -272,7 +275,7 @@ class DeviceEngine:
                 d1[sl] = spec.scale
             h2d(self.d1, d1, self.stream)
             h2d(self.d2, d2, self.stream)
-        torch.cuda.synchronize()
+        self.stream.synchronize()
 
         pk = [KIND_CODE[s.kind] for s in work.primal_cones]
         pd = [s.dim for s in work.primal_cones]

@@ -415,3 +415,17 @@ def test_giant_soc_plain_projection_matches_oracle(P):
         got = e.host(e.py1, p.m)[start:start + dim]
         want = O.proj_soc(np.array(y[start:start + dim]))
         np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * (1 + np.abs(want).max()))
+
+
+def test_solve_many_stress(P):
+    """Many concurrent solves: setup, graph capture and check paths of one
+    engine overlap other threads' work (no device-wide syncs allowed)."""
+    from paper_2603_15504_b200 import instances
+    from paper_2603_15504_b200.batch import solve_many
+
+    probs = [instances.lp_random(400, 800, 0.02, seed) for seed in range(24)]
+    opts = P.SolverOptions(rel_tol=1e-5, abs_tol=1e-5)
+    par = solve_many(probs, opts, max_workers=12)
+    ref = P.solve(probs[7], opts)
+    assert all(r.exit_status == ":optimal" for r in par)
+    np.testing.assert_array_equal(par[7].x, ref.x)

@@ -888,8 +888,9 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const size_t cnt = 2 * (size_t)E->tabY.n_exp;
     if (cudaMalloc(&E->d_exp_rho, sizeof(double) * cnt) != cudaSuccess) return fail(1);
     std::vector<double> nan_init(cnt, NAN);
-    if (cudaMemcpy(E->d_exp_rho, nan_init.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice) !=
-        cudaSuccess)
+    if (cudaMemcpyAsync(E->d_exp_rho, nan_init.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                        s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
       return fail(1);
   }
   E->has_yblocks = E->tabY.total() > 0;
@@ -1168,7 +1169,8 @@ int pdcs_engine_get_ctrl(PdcsEngine* E, PdcsCtrl* h) {
   CK(cudaStreamSynchronize(E->stream));
   std::memcpy(h, E->h_pinned, sizeof(PdcsCtrl));
   int err = 0;
-  CK(cudaMemcpy(&err, E->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(&err, E->d_err, sizeof(int), cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
   if (err && !h->error) h->error = err;
   return 0;
 }

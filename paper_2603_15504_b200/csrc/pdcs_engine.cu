@@ -190,6 +190,20 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   }
   P.vw = choose_vw(nnz, nrows);
   P.long_t = TILE_NNZ;
+  {  // spread of the short rows' lengths (chooses lane-mapped vs tiled step kernels)
+    double s1 = 0.0, s2 = 0.0;
+    int cnt = 0;
+    for (int r = 0; r < nrows; ++r) {
+      const double len = rp[r + 1] - rp[r];
+      if (len > P.long_t) continue;
+      s1 += len;
+      s2 += len * len;
+      ++cnt;
+    }
+    const double mean = cnt ? s1 / cnt : 0.0;
+    const double var = cnt ? std::max(0.0, s2 / cnt - mean * mean) : 0.0;
+    P.len_cv = mean > 0.0 ? std::sqrt(var) / mean : 0.0;
+  }
   // CSR-stream tiles over the short rows: <= TILE_ROWS rows, <= TILE_NNZ entries
   std::vector<int> tiles(1, 0);
   for (int r = 0; r < nrows;) {
@@ -528,7 +542,7 @@ int launch_step_t(Engine* E, const KArgs& A) {
 int step_lanes(int64_t nnz, int64_t nrows) {
   if (nrows <= 0) return 1;
   const double mean = (double)nnz / (double)nrows;
-  return mean <= 6.0 ? 1 : (mean <= 24.0 ? 8 : 32);
+  return mean <= 6.0 ? 1 : (mean <= 64.0 ? 8 : 32);
 }
 
 // the lane-step kernel instance for (lanes per row, GP mode)
@@ -951,12 +965,23 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     E->gp = (int)tune("gp", 0.0) & 1;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
+    auto lanes_knob = [&](const char* key, int dflt) {  // 1, 8 or 32 lanes per row
+      const int v = (int)tune(key, (double)dflt);
+      return v == 1 || v == 8 || v == 32 ? v : dflt;
+    };
+    E->G.step_vw = lanes_knob("vwy", E->G.step_vw);
+    E->GT.step_vw = lanes_knob("vwt", E->GT.step_vw);
     // Measured (profiles/r01_sweeps.txt): thread-per-row lanes win for short
-    // rows (C3, C5); the tiled CSR-stream kernel wins once rows average more
-    // than ~6 entries (C2: 4.7k -> 7.6k it/s, C4's G^T: 3.5k -> 5.0k it/s).
+    // rows (C3, C5); 8 lanes per row win for uniform rows of ~40 (C4's and
+    // C2's G^T: 5.1k -> 5.7k and 8.8k -> 9.2k it/s); the tiled CSR-stream
+    // kernel wins for long-ish rows of very mixed length (C2's G: rows of 1-2
+    // and of ~48 entries).
     const double big = d.nnz >= (1 << 20) ? 1.0 : 0.0;
-    E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1))) > 0.0;
-    E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw > 1))) > 0.0;
+    // G^ x~ rows of mixed length: tiles (C2: 0.044 vs 0.047 ms); G^T y_hat: 8 lanes
+    // even for mixed rows (C2: 0.032 vs 0.048 ms), tiles only where 32 lanes
+    // would be needed
+    E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1 && E->G.len_cv > 0.5))) > 0.0;
+    E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw == 32))) > 0.0;
     if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
       return fail(1);
     if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)

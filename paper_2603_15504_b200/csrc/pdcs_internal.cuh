@@ -21,6 +21,7 @@ struct SpmvPlan {
   const double* val = nullptr;
   int vw = 1;
   int step_vw = 1;  // lanes per row of the fused step kernels (panel rows are shorter)
+  double len_cv = 0.0;  // coefficient of variation of the short rows' lengths
   int long_t = 1 << 30;
   int n_long = 0, n_chunks = 0;
   int* d_long_rows = nullptr;     // [n_long]

@@ -184,28 +184,19 @@ __global__ void k_long_partial(const int4* __restrict__ ch, int nch, const int* 
   CtaGrp g(sh);
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const int4 q = ch[c];
-    // the 16-byte aligned body of the chunk with vector loads (4 columns, 4
-    // values per thread and step), the <= 3 + 3 unaligned ends scalar; four
-    // accumulators (entry index mod 4) keep four gathers in flight
-    const int vb = (q.y + 3) & ~3, ve = max(vb, q.z & ~3);
+    // four independent accumulators keep four gathers in flight per thread
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    for (int gi = (vb >> 2) + threadIdx.x; gi < (ve >> 2); gi += blockDim.x) {
-      const int4 cc = __ldg(reinterpret_cast<const int4*>(ci) + gi);
-      const double2 v01 = __ldg(reinterpret_cast<const double2*>(va) + 2 * gi);
-      const double2 v23 = __ldg(reinterpret_cast<const double2*>(va) + 2 * gi + 1);
-      s0 += v01.x * __ldg(x + cc.x);
-      s1 += v01.y * __ldg(x + cc.y);
-      s2 += v23.x * __ldg(x + cc.z);
-      s3 += v23.y * __ldg(x + cc.w);
+    const int bd = blockDim.x;
+    int j = q.y + threadIdx.x;
+    for (; j + 3 * bd < q.z; j += 4 * bd) {
+      const int c0 = __ldg(ci + j), c1 = __ldg(ci + j + bd), c2 = __ldg(ci + j + 2 * bd),
+                c3 = __ldg(ci + j + 3 * bd);
+      s0 += __ldg(va + j) * __ldg(x + c0);
+      s1 += __ldg(va + j + bd) * __ldg(x + c1);
+      s2 += __ldg(va + j + 2 * bd) * __ldg(x + c2);
+      s3 += __ldg(va + j + 3 * bd) * __ldg(x + c3);
     }
-    const int hn = min(vb, q.z) - q.y, tn = q.z > ve ? q.z - ve : 0;
-    if ((int)threadIdx.x < hn) {
-      const int j = q.y + threadIdx.x;
-      s0 += __ldg(va + j) * __ldg(x + __ldg(ci + j));
-    } else if (threadIdx.x >= 4 && (int)threadIdx.x - 4 < tn) {
-      const int j = ve + threadIdx.x - 4;
-      s0 += __ldg(va + j) * __ldg(x + __ldg(ci + j));
-    }
+    for (; j < q.z; j += bd) s0 += __ldg(va + j) * __ldg(x + __ldg(ci + j));
     const double s = g.sum((s0 + s1) + (s2 + s3));
     if (threadIdx.x == 0) out[c] = s;
   }

@@ -76,6 +76,19 @@ def test_long_rows_spmv(P):
     np.testing.assert_allclose(A.rmatvec(y), A._csr.T.tocsr() @ y, rtol=1e-11, atol=1e-10)
 
 
+def test_dense_long_rows_spmv(P):
+    """Fully dense long rows (the factor rows of C4) take the chunk path
+    without column indices."""
+    rng = np.random.default_rng(5)
+    n = 30_000
+    dense = sp.csr_matrix(rng.standard_normal((3, n)))
+    sparse = sp.random(50, n, 0.01, format="csr", random_state=rng, data_rvs=rng.standard_normal)
+    G = sp.vstack([sparse[:20], dense, sparse[20:]]).tocsr()
+    A = P.SparseMatrix(G)
+    x = rng.standard_normal(n)
+    np.testing.assert_allclose(A.matvec(x), G @ x, rtol=1e-11, atol=1e-10)
+
+
 def test_projections_match_golden(P):
     from paper_2603_15504_b200 import cones
 

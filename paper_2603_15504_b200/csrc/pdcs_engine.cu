@@ -683,7 +683,7 @@ int launch_slot(Engine* E) {
     mark(s, "allreduce_xy");
   }
   if (!fuse_ls(E).mode) {
-    k_ctrl_ls<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
+    k_ctrl_ls<<<1, 1024, 0, s>>>(E->d_ctrl, E->d_partX, E->capX, E->d_partY, E->capY, E->d_red,
                                E->comm ? E->d_yred : nullptr);
     CKL();
     mark(s, "ctrl_linesearch");
@@ -722,7 +722,7 @@ int launch_slot(Engine* E) {
     tred = E->d_yred + 8;
   }
   if (!fuse_beta(E).mode) {
-    k_ctrl_beta<<<1, BS, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err, tred);
+    k_ctrl_beta<<<1, 1024, 0, s>>>(E->d_ctrl, E->d_partT, E->capT, E->d_red, E->d_err, tred);
     CKL();
     mark(s, "ctrl_beta");
   }

@@ -31,7 +31,9 @@ struct CtrlFuse {
   double* red;
   const int* err;
 };
+template <int U = 1>
 __device__ void ctrl_ls_body(PdcsCtrl*, const double*, int, const double*, int, double*, const double*);
+template <int U = 1>
 __device__ void ctrl_beta_body(PdcsCtrl*, const double*, int, const double*, const int*,
                                const double*);
 __device__ __forceinline__ void fused_ctrl(const CtrlFuse& F);
@@ -1127,15 +1129,35 @@ __global__ void __launch_bounds__(BS, 8) k_step_t_lane(KArgs A, int nrows, TileS
 // Sums of NQ partial rows p[q * cap + 0 .. n) by one CTA: all rows' loads are
 // in flight together and the tree reductions share one pair of barriers.
 // Thread 0 receives the sums (the controllers below run on thread 0).
-template <int NQ>
+template <int NQ, int U = 1>
 __device__ __forceinline__ void cta_sum_rows(const double* p, int cap, int n, double (&out)[NQ]) {
   __shared__ double sh[NQ][32];
+  // U independent accumulator sets keep U NQ L2 loads in flight per thread
+  // (the standalone controllers: U = 4; folded into a step kernel: U = 1, so
+  // the step kernel's register budget is not spent on the controller)
+  double tu[U][NQ];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tu[u][q] = 0.0;
+  const int bd = blockDim.x;
+  int s0 = threadIdx.x;
+  for (; s0 + (U - 1) * bd < n; s0 += U * bd) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) tu[u][q] += __ldcg(p + (size_t)q * cap + s0 + u * bd);  // L2: other CTAs wrote them
+  }
+  for (; s0 < n; s0 += bd) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) tu[0][q] += __ldcg(p + (size_t)q * cap + s0);
+  }
   double t[NQ];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) t[q] = 0.0;
-  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+  for (int q = 0; q < NQ; ++q) {
+    t[q] = tu[0][q];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) t[q] += __ldcg(p + (size_t)q * cap + s);  // L2: other CTAs wrote them
+    for (int u = 1; u < U; ++u) t[q] += tu[u][q];
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -1156,6 +1178,7 @@ __device__ __forceinline__ void cta_sum_rows(const double* p, int cap, int n, do
 
 // Line-search controller (engine.py:183-243), run by one whole CTA.
 // yred (sharded mode): the y-space sums already all-reduced across ranks.
+template <int U>
 __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                              int capY, double* red, const double* yred) {
   double sx[GX_N], sy[GY_N];
@@ -1165,8 +1188,8 @@ __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const d
 #pragma unroll
     for (int q = 0; q < GX_N; ++q) sx[q] = yred[GY_N + q];
   } else {
-    cta_sum_rows<GX_N>(partX, capX, capX, sx);
-    cta_sum_rows<GY_N>(partY, capY, capY, sy);
+    cta_sum_rows<GX_N, U>(partX, capX, capX, sx);
+    cta_sum_rows<GY_N, U>(partY, capY, capY, sy);
   }
   if (threadIdx.x != 0) return;
   const double xx = sx[GX_XX], dxdx = sx[GX_DXDX], cx = sx[GX_CX];
@@ -1229,12 +1252,13 @@ __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const d
 __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                           int capY, double* red, const double* yred) {
   if (C->stop) return;
-  ctrl_ls_body(C, partX, capX, partY, capY, red, yred);
+  ctrl_ls_body<4>(C, partX, capX, partY, capY, red, yred);
 }
 
 // Reflection parameter, Halpern coefficients, averaging weight and the stop
 // tests of an accepted iteration (engine.py:590-628, termination.py:150-160),
 // run by one whole CTA.
+template <int U>
 __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const double* red,
                                const int* err, const double* tred) {
   double st[GT_N];
@@ -1242,7 +1266,7 @@ __device__ void ctrl_beta_body(PdcsCtrl* C, const double* partT, int capT, const
 #pragma unroll
     for (int q = 0; q < GT_N; ++q) st[q] = tred[q];
   } else {
-    cta_sum_rows<GT_N>(partT, capT, capT, st);
+    cta_sum_rows<GT_N, U>(partT, capT, capT, st);
   }
   if (threadIdx.x != 0) return;
   const double rd2 = st[GT_RD2], ls = st[GT_LSUM], us = st[GT_USUM];
@@ -1307,7 +1331,7 @@ __global__ void k_err_to_double(const int* err, double* out) { *out = (double)*e
 __global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
                             const int* err, const double* tred) {
   if (C->stop || !C->accepted) return;
-  ctrl_beta_body(C, partT, capT, red, err, tred);
+  ctrl_beta_body<4>(C, partT, capT, red, err, tred);
 }
 
 // Controller folded into the last CTA of the kernel that writes the final
@@ -1326,8 +1350,8 @@ __device__ __forceinline__ bool last_cta(unsigned* ticket) {
 
 __device__ __forceinline__ void fused_ctrl(const CtrlFuse& F) {
   if (!F.mode || !last_cta(F.ticket)) return;
-  if (F.mode == 1) ctrl_ls_body(F.C, F.partA, F.capA, F.partB, F.capB, F.red, nullptr);
-  else ctrl_beta_body(F.C, F.partB, F.capB, F.red, F.err, nullptr);
+  if (F.mode == 1) ctrl_ls_body<1>(F.C, F.partA, F.capA, F.partB, F.capB, F.red, nullptr);
+  else ctrl_beta_body<1>(F.C, F.partB, F.capB, F.red, F.err, nullptr);
   if (threadIdx.x == 0) *F.ticket = 0u;
 }
 

@@ -442,3 +442,44 @@ def test_solve_many_stress(P):
     ref = P.solve(probs[7], opts)
     assert all(r.exit_status == ":optimal" for r in par)
     np.testing.assert_array_equal(par[7].x, ref.x)
+
+
+@pytest.mark.parametrize("case", ["no_rows", "zero_matrix", "free_vars_soc", "single_row"])
+def test_degenerate_instances_match_oracle(P, case):
+    """Edge shapes: no constraint rows, an all-zero G, free variables bound
+    only through an SOC, a single constraint row.  Same status as the oracle
+    and objectives within the tolerance."""
+    from paper_2603_15504_b200 import Cone, ConeSpec, ConicProblem, SparseMatrix
+
+    rng = np.random.default_rng(11)
+    if case == "no_rows":
+        n = 50
+        p = ConicProblem(c=rng.standard_normal(n), G=SparseMatrix(sp.csr_matrix((0, n))),
+                         h=np.zeros(0), l=-np.ones(n), u=np.ones(n), num_box=n, dual_cones=())
+    elif case == "zero_matrix":
+        n, m = 40, 20
+        p = ConicProblem(c=rng.standard_normal(n), G=SparseMatrix(sp.csr_matrix((m, n))),
+                         h=-np.ones(m), l=-2 * np.ones(n), u=2 * np.ones(n), num_box=n,
+                         dual_cones=(ConeSpec(Cone.NONNEG, m),))
+    elif case == "free_vars_soc":
+        # min c.x s.t. (1, x) in SOC: ||x|| <= 1 -> x* = -c/||c||
+        n = 30
+        G = sp.vstack([sp.csr_matrix((1, n)), sp.identity(n, format="csr")]).tocsr()
+        h = np.concatenate([[-1.0], np.zeros(n)])
+        p = ConicProblem(c=rng.standard_normal(n), G=SparseMatrix(G), h=h, l=np.full(n, -np.inf),
+                         u=np.full(n, np.inf), num_box=n, dual_cones=(ConeSpec(Cone.SOC, n + 1),))
+    else:
+        n = 25
+        G = sp.csr_matrix(np.abs(rng.standard_normal((1, n))))
+        p = ConicProblem(c=np.abs(rng.standard_normal(n)), G=SparseMatrix(G), h=np.array([1.0]),
+                         l=np.zeros(n), u=np.full(n, np.inf), num_box=n,
+                         dual_cones=(ConeSpec(Cone.NONNEG, 1),))
+    opts = dict(rel_tol=1e-6, abs_tol=1e-6, max_iter=200_000)
+    r = P.solve(p, P.SolverOptions(**opts))
+    o = O.solve(O.as_oproblem(p), O.options_from(None, **opts))
+    assert r.exit_status == o["status"], (r.exit_status, o["status"])
+    if r.exit_status == ":optimal":
+        assert abs(r.p_obj - o["p_obj"]) <= 1e-4 * (1 + abs(o["p_obj"]))
+    if case == "free_vars_soc":
+        c = p.c
+        np.testing.assert_allclose(r.x, -c / np.linalg.norm(c), atol=1e-4)

@@ -945,12 +945,13 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       if (p == std::string::npos || (p > 0 && s[p - 1] != ',')) return dflt;
       return atof(s.c_str() + p + k.size());
     };
-    // Column panels: cut the gathered vector into slices of about 1/3 of L2.
+    // Column panels: cut the gathered vector into slices of at most ~0.42 L2.
     // Random 8-byte gathers stay L2-rate bound only while their footprint is
     // below ~50 MB on B200 (tools/gather_probe.cu: 267 G/s up to 48 MB, 196 at
-    // 80 MB, 90 at 160 MB); C5 measured best at 4 panels for G^ x~ (160 MB)
-    // and 2 for G^T y_hat (80 MB) once the passes ran at full occupancy.
-    const double budget = tune("panel_mb", 0.32 * l2 / 1048576.0) * 1048576.0;
+    // 80 MB, 90 at 160 MB); each extra panel costs a partial-sum round trip.
+    // C5 measured best at 3 panels for G^ x~ (160 MB) and 2 for G^T y_hat
+    // (80 MB): 692 it/s against 684 with 4 and 2 (profiles/r01_sweeps.txt).
+    const double budget = tune("panel_mb", 0.42 * l2 / 1048576.0) * 1048576.0;
     auto panels_for = [&](int ncols, int nrows, int nnz) {
       if (nnz < (1 << 20)) return 1;  // small matrices: the whole vector is L2-resident
       int np = (int)std::ceil(8.0 * ncols / budget);

@@ -483,3 +483,23 @@ def test_degenerate_instances_match_oracle(P, case):
     if case == "free_vars_soc":
         c = p.c
         np.testing.assert_allclose(r.x, -c / np.linalg.norm(c), atol=1e-4)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_full_size_trajectory_matches_oracle(P, cfg):
+    """Benchmark-size instances (C2: 5M nnz with 10k SOC blocks; C4: 21M nnz
+    with 41 dense rows and a 500k-row SOC block): the first PDHG iterates of
+    the device engine against the CPU oracle (seconds of numpy per
+    iteration).  C3's million exponential-cone blocks are too slow for the
+    oracle at full size; test_exp_blocks_trajectory_matches_oracle covers
+    them at 3k blocks."""
+    from paper_2603_15504_b200 import instances
+
+    p = instances.CONFIGS[cfg]()
+    kb = tuple(range(1, 7))  # k_bar also counts line-search rejections: compare what both saw
+    dev, orc = _trajectory(P, p, dict(max_iter=6, rel_tol=1e-14, abs_tol=1e-14), kb)
+    assert sorted(dev) == sorted(orc) and len(dev) >= 2, (sorted(dev), sorted(orc))
+    for k in dev:
+        for a, b in zip(dev[k], orc[k]):
+            scale = max(1.0, float(np.max(np.abs(b))))
+            assert np.max(np.abs(a - b)) <= 1e-10 * scale, (cfg, k, np.max(np.abs(a - b)))

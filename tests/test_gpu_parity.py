@@ -485,10 +485,11 @@ def test_degenerate_instances_match_oracle(P, case):
         np.testing.assert_allclose(r.x, -c / np.linalg.norm(c), atol=1e-4)
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C4"])
+@pytest.mark.parametrize("cfg", ["C2", "C4", "C5"])
 def test_full_size_trajectory_matches_oracle(P, cfg):
     """Benchmark-size instances (C2: 5M nnz with 10k SOC blocks; C4: 21M nnz
-    with 41 dense rows and a 500k-row SOC block): the first PDHG iterates of
+    with 41 dense rows and a 500k-row SOC block; C5: the 50M-nnz LP with
+    column panels): the first PDHG iterates of
     the device engine against the CPU oracle (seconds of numpy per
     iteration).  C3's million exponential-cone blocks are too slow for the
     oracle at full size; test_exp_blocks_trajectory_matches_oracle covers

@@ -413,9 +413,27 @@ __device__ inline void proj_exp3(double r, double s, double t, double* o, int* e
     o[0] = vp0; o[1] = vp1; o[2] = vp2;
     return;
   }
-  double lo, hi;
-  exp_bracket(r, s, t, pdist, ddist, lo, hi);
-  double rho = exp_root(r, s, t, lo, hi, rho_io ? *rho_io : NAN);
+  double rho = NAN;
+  if (rho_io && isfinite(*rho_io)) {
+    // warm start: up to 3 plain Newton steps from the previous trial's root;
+    // on convergence (the reference's own stopping tests) the bracket is not
+    // needed -- the root of h in the bracket is unique
+    double x = *rho_io;
+    for (int i = 0; i < 3; ++i) {
+      double f, df;
+      exp_hdh(r, s, t, x, f, df);
+      if (!isfinite(f) || !(df >= 1e-13)) break;
+      if (fabs(f) <= 1e-15) { rho = x; break; }
+      const double xn = x - f / df;
+      if (fabs(xn - x) <= 1e-15 * dmax(1.0, fabs(xn))) { rho = xn; break; }
+      x = xn;
+    }
+  }
+  if (!isfinite(rho)) {
+    double lo, hi;
+    exp_bracket(r, s, t, pdist, ddist, lo, hi);
+    rho = exp_root(r, s, t, lo, hi, rho_io ? *rho_io : NAN);
+  }
   if (rho_io) *rho_io = rho;
   double pr[3], dr;
   if (exp_from_rho(r, s, t, rho, pr, &dr) && dr <= pdist) {

@@ -190,21 +190,65 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   }
   P.vw = choose_vw(nnz, nrows);
   P.long_t = TILE_NNZ;
-  {  // spread of the short rows' lengths (chooses lane-mapped vs tiled step kernels)
+  // one host pass: the spread of the short rows' lengths (chooses lane-mapped
+  // vs tiled step kernels) and the long rows
+  std::vector<int> lrows;
+  {
     double s1 = 0.0, s2 = 0.0;
     int cnt = 0;
     for (int r = 0; r < nrows; ++r) {
-      const double len = rp[r + 1] - rp[r];
-      if (len > P.long_t) continue;
+      const int len = rp[r + 1] - rp[r];
+      if (len > P.long_t) {
+        lrows.push_back(r);
+        continue;
+      }
       s1 += len;
-      s2 += len * len;
+      s2 += (double)len * len;
       ++cnt;
     }
     const double mean = cnt ? s1 / cnt : 0.0;
     const double var = cnt ? std::max(0.0, s2 / cnt - mean * mean) : 0.0;
     P.len_cv = mean > 0.0 ? std::sqrt(var) / mean : 0.0;
   }
-  // CSR-stream tiles over the short rows: <= TILE_ROWS rows, <= TILE_NNZ entries
+  // entries per long-row chunk (one CTA reduction each); PDCS_TUNE=chunk=N overrides
+  int chunk = 8192;
+  if (const char* env = getenv("PDCS_TUNE")) {
+    const char* p = strstr(env, "chunk=");
+    if (p && (p == env || p[-1] == ',')) chunk = std::max(256, atoi(p + 6));
+  }
+  std::vector<int> lfirst;
+  std::vector<int4> chunks;
+  for (int r : lrows) {
+    const int b = rp[r], e = rp[r + 1];
+    lfirst.push_back((int)chunks.size());
+    for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), 0));
+  }
+  lfirst.push_back((int)chunks.size());
+  P.n_long = (int)lrows.size();
+  P.n_chunks = (int)chunks.size();
+  if (P.n_long > 0) {
+    CK(cudaMalloc(&P.d_long_rows, sizeof(int) * P.n_long));
+    CK(cudaMalloc(&P.d_long_first, sizeof(int) * (P.n_long + 1)));
+    CK(cudaMalloc(&P.d_chunks, sizeof(int4) * P.n_chunks));
+    CK(cudaMalloc(&P.d_chunk_out, sizeof(double) * P.n_chunks));
+    CK(cudaMemcpyAsync(P.d_long_rows, lrows.data(), sizeof(int) * P.n_long, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P.d_long_first, lfirst.data(), sizeof(int) * (P.n_long + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(P.d_chunks, chunks.data(), sizeof(int4) * P.n_chunks, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  P.grid = grid_for(nrows, BS / P.vw);
+  return 0;
+}
+
+// CSR-stream tiles over the short rows (<= TILE_ROWS rows, <= TILE_NNZ
+// entries): only built when the tiled step kernels are chosen.
+int build_tiles(SpmvPlan& P, cudaStream_t s) {
+  const int nrows = P.nrows;
+  std::vector<int> rp(nrows + 1, 0);
+  if (nrows > 0) {
+    CK(cudaMemcpyAsync(rp.data(), P.rowptr, sizeof(int) * (nrows + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
   std::vector<int> tiles(1, 0);
   for (int r = 0; r < nrows;) {
     int nz = 0, cnt = 0;
@@ -222,36 +266,6 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   CK(cudaMalloc(&P.d_tiles, sizeof(int) * tiles.size()));
   CK(cudaMemcpyAsync(P.d_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
-  // entries per long-row chunk (one CTA reduction each); PDCS_TUNE=chunk=N overrides
-  int chunk = 8192;
-  if (const char* env = getenv("PDCS_TUNE")) {
-    const char* p = strstr(env, "chunk=");
-    if (p && (p == env || p[-1] == ',')) chunk = std::max(256, atoi(p + 6));
-  }
-  std::vector<int> lrows, lfirst;
-  std::vector<int4> chunks;
-  for (int r = 0; r < nrows; ++r) {
-    const int b = rp[r], e = rp[r + 1];
-    if (e - b > P.long_t) {
-      lrows.push_back(r);
-      lfirst.push_back((int)chunks.size());
-      for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), 0));
-    }
-  }
-  lfirst.push_back((int)chunks.size());
-  P.n_long = (int)lrows.size();
-  P.n_chunks = (int)chunks.size();
-  if (P.n_long > 0) {
-    CK(cudaMalloc(&P.d_long_rows, sizeof(int) * P.n_long));
-    CK(cudaMalloc(&P.d_long_first, sizeof(int) * (P.n_long + 1)));
-    CK(cudaMalloc(&P.d_chunks, sizeof(int4) * P.n_chunks));
-    CK(cudaMalloc(&P.d_chunk_out, sizeof(double) * P.n_chunks));
-    CK(cudaMemcpyAsync(P.d_long_rows, lrows.data(), sizeof(int) * P.n_long, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(P.d_long_first, lfirst.data(), sizeof(int) * (P.n_long + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(P.d_chunks, chunks.data(), sizeof(int4) * P.n_chunks, cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  P.grid = grid_for(nrows, BS / P.vw);
   return 0;
 }
 
@@ -983,6 +997,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // would be needed
     E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1 && E->G.len_cv > 0.5))) > 0.0;
     E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw == 32))) > 0.0;
+    if ((E->tile_y && build_tiles(E->G, s)) || (E->tile_t && build_tiles(E->GT, s))) return fail(1);
     if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
       return fail(1);
     if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)

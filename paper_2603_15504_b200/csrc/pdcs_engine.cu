@@ -482,7 +482,7 @@ int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* 
 // collective) follows them in the slot.
 CtrlFuse fuse_ls(const Engine* E) {
   CtrlFuse F{};
-  if (E->comm || E->has_yblocks) return F;
+  if (E->comm || E->has_yblocks || !E->fuse_ctrl) return F;
   F.mode = 1; F.ticket = E->d_ticket; F.C = E->d_ctrl;
   F.partA = E->d_partX; F.capA = E->capX; F.partB = E->d_partY; F.capB = E->capY;
   F.red = E->d_red; F.err = E->d_err;
@@ -490,7 +490,7 @@ CtrlFuse fuse_ls(const Engine* E) {
 }
 CtrlFuse fuse_beta(const Engine* E) {
   CtrlFuse F{};
-  if (E->comm || E->has_xblocks) return F;
+  if (E->comm || E->has_xblocks || !E->fuse_ctrl) return F;
   F.mode = 2; F.ticket = E->d_ticket + 1; F.C = E->d_ctrl;
   F.partB = E->d_partT; F.capB = E->capT; F.red = E->d_red; F.err = E->d_err;
   return F;
@@ -978,6 +978,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // L2::64B).  Measured slower on C5, as were two rows per thread and
     // loading the epilogue operands ahead of the gathers (profiles/r01_sweeps.txt).
     E->gp = (int)tune("gp", 0.0) & 1;
+    E->fuse_ctrl = tune("fuse", 1.0) > 0.0;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
     auto lanes_knob = [&](const char* key, int dflt) {  // 1, 8 or 32 lanes per row

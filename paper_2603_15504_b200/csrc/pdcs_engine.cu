@@ -455,8 +455,6 @@ TileSrc tile_source(const SpmvPlan& P, const PanelPlan& Q, int p, const double* 
   S.wpart = p > 0 ? wpart : nullptr;
   S.orig_rp = (p == Q.np - 1 && P.n_long) ? P.rowptr : nullptr;
   S.long_t = P.long_t;
-  S.pc8 = Q.d_pc8 ? Q.d_pc8 + (size_t)p * P.nrows : nullptr;
-  S.pb = Q.d_pc8 ? Q.d_pb + (size_t)p * ((P.nrows + 31) / 32) : nullptr;
   return S;
 }
 
@@ -587,7 +585,7 @@ const void* step_t_fn(const Engine* E) {
 }
 
 // Panelled copy of a CSR pattern (values filled by refresh_panel_values).
-int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, bool compact, cudaStream_t s) {
+int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
   Q = PanelPlan();
   Q.np = std::max(1, np);
   if (P.nrows == 0) {
@@ -620,27 +618,6 @@ int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, bool compact, cudaStre
   k_panel_scatter<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width,
                                                    Q.d_po, Q.d_pci, Q.d_pperm);
   CKL();
-  if (compact) {
-    // thread-per-row lanes read 8-bit counts + every 32nd offset instead of
-    // int32 offsets (C5: 1.25 B instead of 4 B per row and panel)
-    int* over = nullptr;
-    CK(cudaMalloc(&over, sizeof(int)));
-    CK(cudaMemsetAsync(over, 0, sizeof(int), s));
-    CK(cudaMalloc(&Q.d_pc8, nflat));
-    CK(cudaMalloc(&Q.d_pb, sizeof(int) * (size_t)Q.np * ((P.nrows + 31) / 32)));
-    k_panel_compact<<<grid_for((int64_t)nflat), BS, 0, s>>>(P.nrows, Q.np, Q.d_po, Q.d_pc8, Q.d_pb, over);
-    CKL();
-    int h_over = 0;
-    CK(cudaMemcpyAsync(&h_over, over, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    cudaFree(over);
-    if (h_over) {
-      cudaFree(Q.d_pc8);
-      cudaFree(Q.d_pb);
-      Q.d_pc8 = nullptr;
-      Q.d_pb = nullptr;
-    }
-  }
   CK(cudaStreamSynchronize(s));
   return 0;
 }
@@ -657,8 +634,6 @@ void free_panels(PanelPlan& Q) {
   cudaFree(Q.d_pci);
   cudaFree(Q.d_pva);
   cudaFree(Q.d_pperm);
-  cudaFree(Q.d_pc8);
-  cudaFree(Q.d_pb);
   Q = PanelPlan();
 }
 
@@ -998,9 +973,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     };
     const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
     const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
-    // c8=0: thread-per-row lanes read int32 panel offsets instead of 8-bit counts
-    const bool c8 = tune("c8", 1.0) > 0.0;
-    if (build_panels(E->PG, E->G, py, c8, s) || build_panels(E->PGT, E->GT, pt, c8, s)) return fail(1);
+    if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
     // gp=1: gathers of the lane-mapped step SpMVs fetch 64 B into L2 (PTX
     // L2::64B).  Measured slower on C5, as were two rows per thread and
     // loading the epilogue operands ahead of the gathers (profiles/r01_sweeps.txt).

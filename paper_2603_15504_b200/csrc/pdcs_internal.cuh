@@ -49,8 +49,6 @@ struct PanelPlan {
   double* d_pva = nullptr;  // [nnz_short]
   int* d_pperm = nullptr;   // [nnz_short] position in the CSR
   int nnz_short = 0;
-  unsigned char* d_pc8 = nullptr;  // [np*nrows] 8-bit entry counts (nullptr: a count exceeds 255)
-  int* d_pb = nullptr;             // [np][ceil(nrows/32)] offset of every 32nd row
 };
 
 // Cone-block table of one space split into size classes.

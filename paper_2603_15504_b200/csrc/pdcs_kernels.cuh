@@ -251,22 +251,6 @@ __global__ void k_panel_scatter(int nrows, const int* __restrict__ rp, const int
   }
 }
 
-// Compact panel offsets: 8-bit counts (po differences) and every 32nd row's
-// offset per panel; *over is set when a count does not fit in 8 bits.
-__global__ void k_panel_compact(int nrows, int np, const int* __restrict__ po, unsigned char* pc8, int* pb,
-                                int* over) {
-  const long long nflat = (long long)np * nrows;
-  const int ng = (nrows + 31) >> 5;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nflat;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c = po[i + 1] - po[i];
-    if (c > 255) *over = 1;
-    pc8[i] = (unsigned char)min(c, 255);
-    const int p = (int)(i / nrows), r = (int)(i - (long long)p * nrows);
-    if ((r & 31) == 0) pb[(long long)p * ng + (r >> 5)] = po[i];
-  }
-}
-
 // Row reductions used by the preconditioner: OP 0 = max |a_ij| (order free),
 // OP 1 = sum |a_ij| (sequential in index order, like scipy's csr sum).
 template <int OP>
@@ -693,12 +677,6 @@ struct TileSrc {
   const double* wpart;  // partial sums of the previous passes (nullptr: start at 0)
   const int* orig_rp;   // rows longer than long_t in the CSR take longv (nullptr: none)
   int long_t;
-  // compact row offsets of this pass for thread-per-row lanes (nullptr: use po):
-  // 8-bit entry counts per row plus the offset of every 32nd row; a warp
-  // rebuilds its 32 rows' offsets with a shuffle scan (1 B instead of 4 B per
-  // row and panel from HBM)
-  const unsigned char* pc8;
-  const int* pb;
 };
 
 __device__ __forceinline__ double tile_rows(const TileSrc& S, const double* __restrict__ x,
@@ -1042,25 +1020,7 @@ __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __res
   constexpr bool H = false;
   int b = 0, e = 0;
   double s = 0.0;
-  if (VW == 1 && S.pc8) {
-    // the warp holds rows base .. base+31 (base a multiple of 32): offsets from
-    // the 8-bit counts by an inclusive shuffle scan (long rows count 0 here)
-    const int lane = threadIdx.x & 31;
-    const int c = r < nrows ? (int)__ldg(S.pc8 + r) : 0;
-    int inc = c;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += t;
-    }
-    b = __ldg(S.pb + (r >> 5)) + inc - c;
-    e = b + c;
-    if (r < nrows) {
-      const bool lng = S.orig_rp && (__ldg(S.orig_rp + r + 1) - __ldg(S.orig_rp + r)) > S.long_t;
-      if (lng) s = longv[r];
-      else if (S.wpart) s = S.wpart[r];
-    }
-  } else if (r < nrows) {
+  if (r < nrows) {
     const bool lng = S.orig_rp && (__ldg(S.orig_rp + r + 1) - __ldg(S.orig_rp + r)) > S.long_t;
     if (lng) {
       if (sub == 0) s = longv[r];

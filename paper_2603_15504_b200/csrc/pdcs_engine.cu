@@ -441,6 +441,30 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
   return 0;
 }
 
+// Launch of a step kernel of the trial; with pdl (E->pdl) as a programmatic
+// dependent launch: the kernel's CTAs are scheduled while the previous
+// kernel's last CTAs (and its folded controller) finish, and wait in
+// pdl_enter() for its completion.
+template <typename... KP, typename... Args>
+cudaError_t launch_step(bool pdl, void (*k)(KP...), int grid, cudaStream_t s, Args... args) {
+  if (!pdl) {
+    k<<<grid, BS, 0, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(BS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+bool use_pdl(const Engine* E) { return E->pdl && !E->comm; }
+
 // ---- one line-search trial (graph slot) ----------------------------------
 // Final-pass source of a fused step SpMV: the last panel (after np-1 partial
 // passes into wpart) or the whole CSR.
@@ -471,8 +495,8 @@ template <int VW, int GP>
 int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* x, double* wpart,
                 int gate, float keep) {
   for (int p = 0; p + 1 < Q.np; ++p) {
-    k_lane_pass<VW, GP><<<P.pass_grid, BS, 0, E->stream>>>(tile_source(P, Q, p, wpart), P.nrows, x,
-                                                          wpart, E->d_ctrl, gate, keep);
+    CK(launch_step(use_pdl(E), k_lane_pass<VW, GP>, P.pass_grid, E->stream, tile_source(P, Q, p, wpart),
+                   P.nrows, x, wpart, (const PdcsCtrl*)E->d_ctrl, gate, keep));
     CKL();
   }
   return 0;
@@ -499,9 +523,8 @@ CtrlFuse fuse_beta(const Engine* E) {
 template <int VW, int GP>
 int lane_y(Engine* E, const KArgs& A) {
   if (lane_passes<VW, GP>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
-  k_step_y_lane<VW, GP><<<E->G.grid, BS, 0, E->stream>>>(
-      A, E->G.nrows, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY,
-      fuse_ls(E));
+  CK(launch_step(use_pdl(E), k_step_y_lane<VW, GP>, E->G.grid, E->stream, A, E->G.nrows,
+                 tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY, fuse_ls(E)));
   CKL();
   return 0;
 }
@@ -509,9 +532,9 @@ int lane_y(Engine* E, const KArgs& A) {
 template <int VW, int GP>
 int lane_t(Engine* E, const KArgs& A) {
   if (lane_passes<VW, GP>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
-  k_step_t_lane<VW, GP><<<E->GT.grid, BS, 0, E->stream>>>(
-      A, E->GT.nrows, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT,
-      fuse_beta(E));
+  CK(launch_step(use_pdl(E), k_step_t_lane<VW, GP>, E->GT.grid, E->stream, A, E->GT.nrows,
+                 tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT,
+                 fuse_beta(E)));
   CKL();
   return 0;
 }
@@ -659,7 +682,7 @@ int launch_slot(Engine* E) {
   cudaStream_t s = E->stream;
   BlkParams none{nullptr, nullptr, nullptr, 0, -1};
   // primal candidate
-  k_step_x<false><<<E->gridStepX, BS, 0, s>>>(A, E->d_partX, E->capX);
+  CK(launch_step(use_pdl(E), k_step_x<false>, E->gridStepX, s, A, E->d_partX, E->capX));
   CKL();
   mark(s, "step_x");
   // x-space cone blocks this engine steps (its slice's blocks when sharded)
@@ -979,6 +1002,8 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // loading the epilogue operands ahead of the gathers (profiles/r01_sweeps.txt).
     E->gp = (int)tune("gp", 0.0) & 1;
     E->fuse_ctrl = tune("fuse", 1.0) > 0.0;
+    // pdl=0: the step kernels of a trial are ordinary stream-ordered launches
+    E->pdl = tune("pdl", 1.0) > 0.0;
     E->G.step_vw = step_lanes(E->PG.nnz_short / std::max(1, E->PG.np), d.m);
     E->GT.step_vw = step_lanes(E->PGT.nnz_short / std::max(1, E->PGT.np), d.n);
     auto lanes_knob = [&](const char* key, int dflt) {  // 1, 8 or 32 lanes per row

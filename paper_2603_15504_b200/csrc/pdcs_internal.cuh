@@ -113,6 +113,7 @@ struct Engine {
   bool tile_y = false, tile_t = false;  // step SpMVs: tiled CSR-stream or lane-mapped
   int gp = 0;  // lane-step gathers: 0 plain, 1 with the L2::64B fill hint
   bool fuse_ctrl = true;  // fold the controllers into the last CTA of the step kernels
+  bool pdl = true;        // programmatic dependent launches between the step kernels of a trial
   size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)
   double* d_partC = nullptr;  // check path partials [max(PDCS_NMET, 4 GAP_K)][capC]

@@ -40,6 +40,16 @@ __device__ __forceinline__ void fused_ctrl(const CtrlFuse& F);
 
 // gate: 0 = always run, 1 = skip when stopped, 2 = skip when stopped or the
 // current trial was rejected.
+// Programmatic dependent launch (the step kernels of one trial, launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): wait for the previous
+// kernel's grid to complete and its writes to be visible -- before ANY global
+// access, in every CTA, so completion stays transitive along the stream.  No
+// explicit launch_dependents: the next grid is launched when all of this
+// grid's CTAs have exited (an early trigger placed the next grid's CTAs on
+// the SMs with free slots first and unbalanced the one-wave grids: C5 612 vs
+// 684 it/s).  A no-op for an ordinary launch.
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ bool gated(const PdcsCtrl* c, int gate) {
   if (gate == 0) return false;
   if (c->stop) return true;
@@ -615,6 +625,7 @@ __global__ void __launch_bounds__(CTA_BLOCK_THREADS) k_blk_cta(const PdcsBlock* 
 // 246-277, 602-610).  Cone coordinates are left unprojected for k_blk_*.
 template <bool H>
 __global__ void __launch_bounds__(BS, 8) k_step_x(KArgs A, double* part, int cap) {
+  pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   // the Halpern / step coefficients live in shared memory (register pressure)
@@ -1066,6 +1077,7 @@ template <int VW, int GP>
 __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const double* __restrict__ x,
                                                   double* wout, const PdcsCtrl* ctrl, int gate,
                                                   float keep) {
+  pdl_enter();
   if (gated(ctrl, gate)) return;
   const uint64_t ps = policy_stream(), pk = policy_keep_frac(keep);
   const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
@@ -1082,6 +1094,7 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
 template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 6) k_step_y_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap, CtrlFuse F) {
+  pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   // the Halpern / step coefficients live in shared memory, not in 16
@@ -1109,6 +1122,7 @@ __global__ void __launch_bounds__(BS, 6) k_step_y_lane(KArgs A, int nrows, TileS
 template <int VW, int GP>
 __global__ void __launch_bounds__(BS, 8) k_step_t_lane(KArgs A, int nrows, TileSrc S, double* part,
                                                        int cap, CtrlFuse F) {
+  pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
   const uint64_t ps = policy_stream(), pky = policy_keep_frac(A.keep_yh);

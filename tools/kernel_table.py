@@ -1,4 +1,4 @@
-"""Per-kernel table of an ncu launch list (the format of profiles/r01_kernels_C1-C4.txt).
+"""Per-kernel table of an ncu launch list (the format of profiles/r01_kernels_C1-C5.txt).
 
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
 sm__warps_active.avg.pct_of_peak_sustained_active --clock-control none \

@@ -64,6 +64,10 @@ def parse_args():
                     help="N>1: every rank solves its own copy instead of one row-sharded solve")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded engine even on one GPU (NCCL in-graph path)")
+    ap.add_argument("--no-ttt-c1", action="store_true",
+                    help="skip the C1 time-to-1e-6 solve (both arms run it by default)")
+    ap.add_argument("--no-sustained", action="store_true",
+                    help="skip the sustained it/s over one whole check interval")
     ap.add_argument("--batch", type=int, default=0,
                     help="also time B concurrent solves of the workload (solve_many) and report the "
                          "aggregate iterations/s (small configurations)")
@@ -160,12 +164,54 @@ def kernel_bytes(problem, stage: str) -> int:
     return 0
 
 
+def workload_config(args, problem) -> dict:
+    """The `config` dict both arms emit (identical for the same workload)."""
+    return {"workload": WORKLOADS[args.config][0], "nnz": int(problem.G.nnz), "m": int(problem.m),
+            "n": int(problem.n),
+            "options": "defaults except rel/abs tol 1e-12 (no early exit)",
+            "l2": "inputs larger than L2 (1.3 GB CSR of G and G^T vs 126 MB L2); no flush needed"}
+
+
+def host_info() -> dict:
+    """CPU model, core count and the numpy/scipy versions."""
+    import numpy
+    import scipy
+
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except AttributeError:
+        avail = os.cpu_count()
+    return {"cpu_model": model, "nproc": os.cpu_count(), "cpus_available": avail,
+            "numpy": numpy.__version__, "scipy": scipy.__version__}
+
+
+def blas_threads() -> int | None:
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else None
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def run_reference(args, rank, world):
-    """The reference arm: the CPU oracle port on the host cores, rank 0 only."""
+    """The reference arm: the CPU oracle port of conic_pdhg (pinned to the
+    reference's golden outputs, tests/test_oracle_golden.py) on the box's host
+    cores, rank 0 only, BLAS left at all the threads it can use.  scipy's
+    csr_matvec and the per-block projections are single-threaded whatever the
+    thread count, so the SpMV-bound iteration runs on one core in practice."""
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import pdcs_oracle as oracle
     from paper_2603_15504_b200 import instances
 
@@ -176,21 +222,37 @@ def run_reference(args, rank, world):
     iters = 3 if args.config in ("C3", "C4", "C5") else min(max(args.steps, 3), 200)
     med, setup = oracle.time_iterations(problem, iters)
     value = 1.0 / med
-    threads = int(os.environ.get("OMP_NUM_THREADS", "0") or 0) or os.cpu_count()
+    host = host_info()
+    threads = blas_threads()
+    cores = host["cpus_available"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * med,
+        # the iterations actually timed (a bounded sample: C5 runs ~2.5 s per iteration on one core)
+        "steps": iters, "steps_requested": args.steps, "warmup": 0, "warmup_requested": args.warmup,
+        "ms_per_step": 1000.0 * med,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": desc, "parallelism": "host"},
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "port",
+        "data": "synthetic", "config": workload_config(args, problem),
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "port",
                          "sample": f"{iters} PDHG iterations of {args.config} by the numpy/scipy oracle "
                                    f"restatement of conic_pdhg (identity scaling, restarts off; "
                                    f"marginal it/s = 1/median iteration time); setup {setup:.1f}s, "
-                                   f"instance generation {gen_s:.1f}s; host threads available {threads}, "
-                                   "scipy csr_matvec and the projections are single-threaded"},
+                                   f"instance generation {gen_s:.1f}s; BLAS threads {threads} of "
+                                   f"{cores} host cores, scipy csr_matvec and the projections are "
+                                   "single-threaded"},
+        "host": host,
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if not args.no_ttt_c1:
+        # C1 to 1e-6 by the same port: the time-to-tolerance the GPU arm's
+        # "time_to_1e-6_C1" is compared with (reference: 46.1 s)
+        from paper_2603_15504_b200 import instances as I
+
+        p1 = I.lp_random(2000, 4000, 0.01, 0)
+        t0 = time.perf_counter()
+        r = oracle.solve(p1, oracle.options_from(None, rel_tol=1e-6, abs_tol=1e-6, time_limit=1e4))
+        line["time_to_1e-6_C1"] = {"status": r["status"], "iterations": int(r["iterations"]),
+                                   "wall_s": time.perf_counter() - t0, "p_obj": float(r["p_obj"])}
     emit(line)
 
 
@@ -260,6 +322,36 @@ def run_ours(args, rank, world, local):
         total_iters = iters
     value = total_iters / (ms / 1000.0)
 
+    # sustained rate over one whole check interval: from the
+    # current k_bar through the next check (termination + restart scan, gap
+    # search, possible restart) to the same position one interval later
+    sustained = None
+    if not args.no_sustained:
+        freq = loop.check_freq if hasattr(loop, "check_freq") else 2000
+        kb0 = state.k_bar
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        s0.record(stream)
+        ex = loop._advance(state, ex, until=kb0 + freq)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        sms = s0.elapsed_time(s1)
+        if dist:
+            t = torch.tensor([sms, wall], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sms, wall = float(t[0].item()), float(t[1].item())
+        its = state.k_bar - kb0
+        sustained = {"iterations": its, "checks": 1, "device_ms": sms, "wall_s": wall,
+                     "value": its / (sms / 1000.0), "value_wall": its / wall, "unit": "it/s",
+                     "iteration_roofline_frac": instances.algorithmic_bytes(problem) * its / (sms / 1000.0)
+                     / 1e9 / peaks()[0],
+                     "note": "one whole check interval (k_bar %d -> %d) incl. the termination / restart "
+                             "check, gap search and any restart" % (kb0, state.k_bar)}
+
     # per-stage device times of eager trials (live, CUDA events on the engine stream)
     stages = []
     if args.profile_reps > 0:
@@ -316,15 +408,32 @@ def run_ours(args, rank, world, local):
         ttt = {"status": r.exit_status, "iterations": r.iterations, "wall_s": time.perf_counter() - t0,
                "solve_time_s": r.solve_time_s, "p_obj": r.p_obj}
 
+    ttt_c1 = None
+    if not args.no_ttt_c1 and not sharded and args.config != "C1":
+        # C1 (2000 x 4000 LP) to 1e-6 through the public solve(): the reference
+        # takes 54,000 iterations / 46.1 s (the reference
+        # arm re-times its port on this box as "time_to_1e-6_C1")
+        p1 = instances.lp_random(2000, 4000, 0.01, 0)
+        t0 = time.perf_counter()
+        r1 = solve(p1, SolverOptions(rel_tol=1e-6, abs_tol=1e-6))
+        ttt_c1 = {"status": r1.exit_status, "iterations": r1.iterations, "wall_s": time.perf_counter() - t0,
+                  "solve_time_s": r1.solve_time_s, "p_obj": r1.p_obj,
+                  "reference": {"iterations": 54000, "wall_s": 46.1, "p_obj": -5063.1994466,
+                                "source": "BASELINE.md section 2 (reference conic_pdhg, survey host)"}}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+
         from oracle import pdcs_oracle as oracle
 
         it_cpu = 2 if args.config in ("C3", "C4", "C5") else 20
-        med, setup = oracle.time_iterations(problem, it_cpu)
+        with threadpool_limits(limits=1):
+            med, setup = oracle.time_iterations(problem, it_cpu)
         cpu = {"value": 1.0 / med, "unit": "it/s", "cores": 1, "kind": "port",
                "sample": f"{it_cpu} PDHG iterations of {args.config} by the numpy/scipy oracle restatement "
-                         f"(identity scaling, restarts off; 1/median iteration time; setup {setup:.1f}s)"}
+                         f"(identity scaling, restarts off; 1/median iteration time; setup {setup:.1f}s; "
+                         "BLAS pinned to 1 thread)"}
 
     if rank == 0:
         line = {
@@ -332,14 +441,12 @@ def run_ours(args, rank, world, local):
             "warmup": args.warmup, "ms_per_step": ms / max(iters, 1), "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": desc, "nnz": int(problem.G.nnz), "m": problem.m, "n": problem.n,
-                       "parallelism": (f"sharded x{world}: rows of G and x-slices, in-graph NCCL all-gather of x~ + reduce-scatter of G^T y"
-                                       if sharded else ("replicas" if world > 1 else "single")),
-                       "l2": "inputs larger than L2 (1.3 GB CSR of G and G^T vs 126 MB L2); no flush needed",
-                       "options": "defaults except rel/abs tol 1e-12 (no early exit)",
-                       "iterations_timed": iters, "restarts_so_far": state.t,
-                       "setup_s": setup_s, "instance_gen_s": gen_s, "launch": launch_info,
-                       "tune": os.environ.get("PDCS_TUNE", "")},
+            "config": workload_config(args, problem),
+            "parallelism": (f"sharded x{world}: rows of G and x-slices, in-graph NCCL all-gather of x~ + "
+                            "reduce-scatter of G^T y" if sharded else ("replicas" if world > 1 else "single")),
+            "run": {"iterations_timed": iters, "restarts_so_far": state.t, "setup_s": setup_s,
+                    "instance_gen_s": gen_s, "launch": launch_info, "tune": os.environ.get("PDCS_TUNE", ""),
+                    "host": host_info()},
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom_gbs, "peak": peak,
                          "unit": "GB/s", "frac": dom_gbs / peak,
                          "traffic": measured_traffic(args.config, dom[0]),
@@ -351,6 +458,10 @@ def run_ours(args, rank, world, local):
         }
         if ttt:
             line["time_to_1e-6"] = ttt
+        if ttt_c1:
+            line["time_to_1e-6_C1"] = ttt_c1
+        if sustained:
+            line["sustained"] = sustained
         if batched:
             line["batched"] = batched
         emit(line)

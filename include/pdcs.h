@@ -74,7 +74,8 @@ enum {
   PDCS_ERR_TRIAL_CAP = 2,       /* engine.py:243 */
   PDCS_ERR_EXP_NONFINITE = 3,   /* cones.py:301-302 */
   PDCS_ERR_RSOC_BRACKET = 4,    /* cones.py:395-412 */
-  PDCS_ERR_BETA = 5             /* non-finite reflection parameter */
+  PDCS_ERR_BETA = 5,            /* non-finite reflection parameter */
+  PDCS_ERR_RSOC_ROOT = 6        /* brentq did not converge in max_root_iters (cones.py:414-425) */
 };
 
 /* Control block of the device-resident loop (SolverState, engine.py:94-113,
@@ -155,6 +156,16 @@ int pdcs_transpose_csr(int32_t nrows, int32_t ncols, int32_t nnz, const int32_t*
  * internally).  h_err receives the numerical error code (PDCS_ERR_*). */
 int pdcs_project_segments(int32_t len, const double* d_in, double* d_out, const PdcsBlock* h_blocks,
                           int32_t nblocks, const double* d_scale, int32_t* h_err, void* stream);
+
+/* pdcs_project_segments with explicit root-finding controls: the fields of
+ * ProjectionSettings (cones.py:24-32).  root_tol is the exp-cone bisection
+ * stopping width (cones.py:263); max_root_iters bounds the exp-cone
+ * Newton + bisection evaluations (cones.py:227, 256) and brentq's iterations
+ * of the rescaled SOC (cones.py:421; not converging sets PDCS_ERR_RSOC_ROOT).
+ * pdcs_project_segments uses the defaults (1e-12, 100). */
+int pdcs_project_segments_ex(int32_t len, const double* d_in, double* d_out, const PdcsBlock* h_blocks,
+                             int32_t nblocks, const double* d_scale, double root_tol,
+                             int32_t max_root_iters, int32_t* h_err, void* stream);
 
 /* out = clip(in, l, u) componentwise, NaN-propagating like np.clip
  * (project_box, cones.py:46-51). */
@@ -267,6 +278,10 @@ int pdcs_dot_diff(PdcsEngine* e, int32_t space, const double* d_a, const double*
  * 3 = K_p* on the cone part (x-space positions >= num_box),
  * 4 = K_p on the cone part. */
 int pdcs_project_set(PdcsEngine* e, int32_t which, const double* d_in, double* d_out);
+/* pdcs_project_set with the ProjectionSettings fields (cones.py:24-32; see
+ * pdcs_project_segments_ex); the set functions of cones.py:498-549 take them. */
+int pdcs_project_set_ex(PdcsEngine* e, int32_t which, const double* d_in, double* d_out,
+                        double root_tol, int32_t max_root_iters);
 
 /* out = x - tau (c^ - gty) (space 0) or y + sigma (h^ - w) (space 1): the
  * two pre-projection updates of _pdhg_candidate (engine.py:155-161). */

@@ -86,6 +86,8 @@ _SIGS = {
     "pdcs_transpose_csr": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pdcs_project_segments": (C.c_int, [C.c_int32, _P, _P, C.POINTER(PdcsBlock), C.c_int32, _P,
                                         C.POINTER(C.c_int32), _P]),
+    "pdcs_project_segments_ex": (C.c_int, [C.c_int32, _P, _P, C.POINTER(PdcsBlock), C.c_int32, _P,
+                                           C.c_double, C.c_int32, C.POINTER(C.c_int32), _P]),
     "pdcs_project_box": (C.c_int, [C.c_int32, _P, _P, _P, _P, _P]),
     "pdcs_vec_axpby": (C.c_int, [C.c_int32, C.c_double, _P, C.c_double, _P, C.c_double, _P, _P]),
     "pdcs_engine_create": (C.c_int, [C.POINTER(PdcsEngineDesc), _P, C.POINTER(_P)]),
@@ -108,6 +110,7 @@ _SIGS = {
     "pdcs_dist2": (C.c_int, [_P, C.c_int32, _P, _P, C.POINTER(C.c_double)]),
     "pdcs_dot_diff": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P, C.POINTER(C.c_double)]),
     "pdcs_project_set": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "pdcs_project_set_ex": (C.c_int, [_P, C.c_int32, _P, _P, C.c_double, C.c_int32]),
     "pdcs_step_input": (C.c_int, [_P, C.c_int32, _P, _P, C.c_double, _P]),
     "pdcs_axpby": (C.c_int, [_P, C.c_int32, C.c_double, _P, C.c_double, _P, _P]),
     "pdcs_unscale": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),

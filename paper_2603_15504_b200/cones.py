@@ -20,13 +20,16 @@ from .model import KIND_CODE, Cone
 _ERR_TEXT = {
     3: "exponential-cone projection of a non-finite point",
     4: "rescaled-soc projection failed to bracket the multiplier",
+    6: "rescaled-soc root finding failed to converge within max_root_iters",
 }
 
 
 @dataclass(frozen=True)
 class ProjectionSettings:
-    """Root-finding controls (cones.py:24-32).  The device kernels use the
-    default values; other values are accepted for API compatibility."""
+    """Root-finding controls (cones.py:24-32), honoured by the device kernels:
+    root_tol is the exp-cone bisection width (cones.py:263), max_root_iters
+    bounds the exp-cone Newton + bisection evaluations (cones.py:227, 256)
+    and the rescaled-SOC brentq iterations (cones.py:421)."""
 
     root_tol: float = 1e-12
     max_root_iters: int = 100
@@ -35,11 +38,12 @@ class ProjectionSettings:
 DEFAULT_SETTINGS = ProjectionSettings()
 
 
-def _seg(v, kind_code, smode=N.SCALE_NONE, scale=None):
+def _seg(v, kind_code, smode=N.SCALE_NONE, scale=None, settings: ProjectionSettings = DEFAULT_SETTINGS):
     from .device import project_segments
 
     v = np.asarray(v, dtype=np.float64)
-    out, err = project_segments(v, [(kind_code, 0, v.size, smode)], scale)
+    out, err = project_segments(v, [(kind_code, 0, v.size, smode)], scale,
+                                settings.root_tol, settings.max_root_iters)
     if err:
         raise NumericalError(_ERR_TEXT.get(err, f"projection failure {err}"))
     return out
@@ -84,12 +88,12 @@ def in_dual_exp(v, atol: float = 0.0) -> bool:
 
 def project_exp(v: np.ndarray, settings: ProjectionSettings = DEFAULT_SETTINGS) -> np.ndarray:
     """Exact Euclidean projection onto the exponential cone (cones.py:298-326)."""
-    return _seg(v, N.EXP)
+    return _seg(v, N.EXP, settings=settings)
 
 
 def project_dual_exp(v: np.ndarray, settings: ProjectionSettings = DEFAULT_SETTINGS) -> np.ndarray:
     """Moreau: P_{K*}(v) = v + P_K(-v) (cones.py:329-331)."""
-    return _seg(v, N.DUAL_EXP)
+    return _seg(v, N.DUAL_EXP, settings=settings)
 
 
 def project_rescaled_soc(v: np.ndarray, d: np.ndarray,
@@ -103,7 +107,7 @@ def project_rescaled_soc(v: np.ndarray, d: np.ndarray,
         raise ValueError("scale entries must be strictly positive and finite")
     if np.all(d == d[0]):
         return project_soc(v)
-    return _seg(v, N.SOC, N.SCALE_DIRECT, d)
+    return _seg(v, N.SOC, N.SCALE_DIRECT, d, settings)
 
 
 _DUAL_KIND = {
@@ -133,8 +137,8 @@ def project_cone(v: np.ndarray, kind: Cone, scale: np.ndarray | None = None,
     if kind in (Cone.EXP, Cone.DUAL_EXP) and not uniform:
         raise ValueError(f"{kind.value} blocks support only block-uniform scaling; rebuild the scaling")
     if kind is Cone.SOC and not uniform:
-        return _seg(v, N.SOC, N.SCALE_DIRECT, np.asarray(scale, dtype=np.float64))
-    return _seg(v, KIND_CODE[kind])
+        return _seg(v, N.SOC, N.SCALE_DIRECT, np.asarray(scale, dtype=np.float64), settings)
+    return _seg(v, KIND_CODE[kind], settings=settings)
 
 
 def project_cone_dual(v: np.ndarray, kind: Cone, scale: np.ndarray | None = None,
@@ -144,7 +148,7 @@ def project_cone_dual(v: np.ndarray, kind: Cone, scale: np.ndarray | None = None
     return project_cone(v, dual_cone_kind(kind), inv, settings)
 
 
-def _set(problem, which, v, space_len, offset=0):
+def _set(problem, which, v, space_len, offset=0, settings: ProjectionSettings = DEFAULT_SETTINGS):
     from .device import engine_for
 
     e = engine_for(problem)
@@ -154,30 +158,30 @@ def _set(problem, which, v, space_len, offset=0):
     full = np.zeros(space_len)
     full[offset:offset + v.size] = v
     e.upload(buf_in, full)
-    e.project_set(which, buf_in, buf_out)
+    e.project_set(which, buf_in, buf_out, settings.root_tol, settings.max_root_iters)
     return e.host(buf_out, space_len)[offset:offset + v.size]
 
 
 def project_primal_set(x: np.ndarray, problem, settings: ProjectionSettings = DEFAULT_SETTINGS):
     """Projection onto [l, u] x K_p (cones.py:498-506)."""
-    return _set(problem, 0, x, problem.n)
+    return _set(problem, 0, x, problem.n, settings=settings)
 
 
 def project_dual_set(y: np.ndarray, problem, settings: ProjectionSettings = DEFAULT_SETTINGS):
     """Projection of y onto K_d, the blockwise dual of the stored kinds (cones.py:509-520)."""
-    return _set(problem, 1, y, problem.m)
+    return _set(problem, 1, y, problem.m, settings=settings)
 
 
 def project_dual_residual_set(r: np.ndarray, problem, settings: ProjectionSettings = DEFAULT_SETTINGS):
     """Projection of Gx - h onto K_d* (cones.py:523-530)."""
-    return _set(problem, 2, r, problem.m)
+    return _set(problem, 2, r, problem.m, settings=settings)
 
 
 def project_primal_cone_part(v: np.ndarray, problem, settings: ProjectionSettings = DEFAULT_SETTINGS):
     """Projection of a length n - num_box vector onto K_p (cones.py:533-539)."""
-    return _set(problem, 4, v, problem.n, problem.num_box)
+    return _set(problem, 4, v, problem.n, problem.num_box, settings=settings)
 
 
 def project_primal_cone_dual(lam: np.ndarray, problem, settings: ProjectionSettings = DEFAULT_SETTINGS):
     """Projection of lambda_2 onto K_p* (cones.py:542-549)."""
-    return _set(problem, 3, lam, problem.n, problem.num_box)
+    return _set(problem, 3, lam, problem.n, problem.num_box, settings=settings)

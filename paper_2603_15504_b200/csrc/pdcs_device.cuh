@@ -315,11 +315,22 @@ __device__ inline void exp_bracket(double r, double s, double t, double pdist, d
   hi_out = hi;
 }
 
+// Root-finding controls of the projections (ProjectionSettings, cones.py:24-32):
+// tol = root_tol, iters = max_root_iters.  The solver always uses the defaults
+// (the reference's engine never passes settings); the standalone projection
+// API passes the caller's.
+struct RootCfg {
+  double tol = 1e-12;
+  int iters = 100;
+};
+
 // x0: optional Newton start (the block's root from the previous PDHG trial);
 // NaN or outside (lo, hi) means the reference's midpoint start.
+// cones.py:225-265: min(20, iters) damped Newton steps, then bisection up to
+// `iters` evaluations in total, stopping at tol relative width.
 __device__ inline double exp_root(double r, double s, double t, double lo, double hi,
-                                  double x0 = NAN) {
-  const int newton = 20, total = 100;
+                                  double x0 = NAN, RootCfg rc = RootCfg()) {
+  const int newton = rc.iters < 20 ? rc.iters : 20, total = rc.iters;
   double x = (x0 > lo && x0 < hi) ? x0 : 0.5 * (lo + hi);
   bool done = false;
   for (int i = 0; i < newton; ++i) {
@@ -343,7 +354,7 @@ __device__ inline double exp_root(double r, double s, double t, double lo, doubl
   for (int i = 0; i < total - newton; ++i) {
     x = 0.5 * (lo + hi);
     if (exp_h(r, s, t, x) < 0.0) lo = x; else hi = x;
-    if (hi - lo <= 1e-12 * dmax(1.0, fabs(hi))) break;
+    if (hi - lo <= rc.tol * dmax(1.0, fabs(hi))) break;
   }
   return 0.5 * (lo + hi);
 }
@@ -371,21 +382,25 @@ __device__ inline bool exp_from_rho(double r, double s, double t, double rho, do
   return true;
 }
 
-// Euclidean projection of (r, s, t) onto K_exp (cones.py:298-326).  Sets *err
-// for non-finite input (the reference raises NumericalError).
-// rho_io (optional): warm start for the Newton root-find, updated with the
-// root found -- consecutive PDHG trials project nearby points, so Newton
-// starts next to its root instead of at the bracket midpoint.
-__device__ inline void proj_exp3(double r, double s, double t, double* o, int* err,
-                                 double* rho_io = nullptr) {
+// Cheap cases of the projection onto K_exp (cones.py:298-320): non-finite
+// input (error), member, polar member, the flat piece, and the heuristics'
+// early exit.  Returns true with o set when one of them decides; otherwise
+// leaves the heuristic primal point and both heuristic distances in H for the
+// root stage.
+struct ExpHeur {
+  double vp0, vp1, vp2, pdist, ddist;
+};
+
+__device__ __forceinline__ bool exp_cheap(double r, double s, double t, double* o, int* err,
+                                          ExpHeur& H) {
   if (!(isfinite(r) && isfinite(s) && isfinite(t))) {
     *err = PDCS_ERR_EXP_NONFINITE;
     o[0] = r; o[1] = s; o[2] = t;
-    return;
+    return true;
   }
-  if (exp_member(r, s, t)) { o[0] = r; o[1] = s; o[2] = t; return; }
-  if (dual_exp_member(-r, -s, -t)) { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; return; }
-  if (r <= 0.0 && s <= 0.0) { o[0] = r; o[1] = 0.0; o[2] = t < 0.0 ? 0.0 : t; return; }
+  if (exp_member(r, s, t)) { o[0] = r; o[1] = s; o[2] = t; return true; }
+  if (dual_exp_member(-r, -s, -t)) { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; return true; }
+  if (r <= 0.0 && s <= 0.0) { o[0] = r; o[1] = 0.0; o[2] = t < 0.0 ? 0.0 : t; return true; }
   // primal heuristic (cones.py:102-113)
   double vp0 = dmin(r, 0.0), vp1 = 0.0, vp2 = dmax(t, 0.0);
   double pdist = sqrt((r - vp0) * (r - vp0) + s * s + (t - vp2) * (t - vp2));
@@ -411,44 +426,94 @@ __device__ inline void proj_exp3(double r, double s, double t, double* o, int* e
   double inner = vp0 * vd0 + vp1 * vd1 + vp2 * vd2;
   if (dmin(pdist, ddist) <= tol || (merr <= tol && inner <= tol)) {
     o[0] = vp0; o[1] = vp1; o[2] = vp2;
-    return;
+    return true;
   }
-  double rho = NAN;
-  if (rho_io && isfinite(*rho_io)) {
-    // warm start: up to 3 plain Newton steps from the previous trial's root;
-    // on convergence (the reference's own stopping tests) the bracket is not
-    // needed -- the root of h in the bracket is unique
-    double x = *rho_io;
-    for (int i = 0; i < 3; ++i) {
-      double f, df;
-      exp_hdh(r, s, t, x, f, df);
-      if (!isfinite(f) || !(df >= 1e-13)) break;
-      if (fabs(f) <= 1e-15) { rho = x; break; }
-      const double xn = x - f / df;
-      if (fabs(xn - x) <= 1e-15 * dmax(1.0, fabs(xn))) { rho = xn; break; }
-      x = xn;
-    }
+  H.vp0 = vp0; H.vp1 = vp1; H.vp2 = vp2; H.pdist = pdist; H.ddist = ddist;
+  return false;
+}
+
+// Warm start: up to 3 plain Newton steps from the previous trial's root,
+// with the reference's own stopping tests.  The converged root is used only
+// if it lies inside the cheap bracket bounds (rho >= 1 - s/r for r > 0,
+// rho <= r/s for s > 0, cones.py:200-211) and gives a valid point no farther
+// than the primal heuristic; h's root in the full bracket is unique, so such
+// a root is the one the reference finds.  Returns true (o set, *rho_io
+// updated) on success; anything else goes to exp_rooted.
+__device__ __forceinline__ bool exp_warm(double r, double s, double t, const ExpHeur& H, double* o,
+                                         double* rho_io) {
+  if (!isfinite(*rho_io)) return false;
+  double x = *rho_io, rho = NAN;
+  for (int i = 0; i < 3; ++i) {
+    double f, df;
+    exp_hdh(r, s, t, x, f, df);
+    if (!isfinite(f) || !(df >= 1e-13)) break;
+    if (fabs(f) <= 1e-15) { rho = x; break; }
+    const double xn = x - f / df;
+    if (fabs(xn - x) <= 1e-15 * dmax(1.0, fabs(xn))) { rho = xn; break; }
+    x = xn;
   }
-  if (!isfinite(rho)) {
-    double lo, hi;
-    exp_bracket(r, s, t, pdist, ddist, lo, hi);
-    rho = exp_root(r, s, t, lo, hi, rho_io ? *rho_io : NAN);
-  }
+  if (!isfinite(rho) || (r > 0.0 && rho < 1.0 - s / r) || (s > 0.0 && rho > r / s)) return false;
+  double pr[3], dr;
+  if (!exp_from_rho(r, s, t, rho, pr, &dr) || !(dr <= H.pdist)) return false;
+  *rho_io = rho;
+  o[0] = pr[0]; o[1] = pr[1]; o[2] = pr[2];
+  return true;
+}
+
+// The reference's root stage (cones.py:321-326): bracket, safeguarded Newton
+// + bisection (started from the warm root when it lies inside the bracket),
+// the candidate from the root, else the primal heuristic point.
+__device__ inline void exp_rooted(double r, double s, double t, const ExpHeur& H, double* o,
+                                  double* rho_io, RootCfg rc) {
+  double lo, hi;
+  exp_bracket(r, s, t, H.pdist, H.ddist, lo, hi);
+  const double rho = exp_root(r, s, t, lo, hi, rho_io ? *rho_io : NAN, rc);
   if (rho_io) *rho_io = rho;
   double pr[3], dr;
-  if (exp_from_rho(r, s, t, rho, pr, &dr) && dr <= pdist) {
+  if (exp_from_rho(r, s, t, rho, pr, &dr) && dr <= H.pdist) {
     o[0] = pr[0]; o[1] = pr[1]; o[2] = pr[2];
     return;
   }
-  o[0] = vp0; o[1] = vp1; o[2] = vp2;
+  o[0] = H.vp0; o[1] = H.vp1; o[2] = H.vp2;
+}
+
+// Euclidean projection of (r, s, t) onto K_exp (cones.py:298-326).  Sets *err
+// for non-finite input (the reference raises NumericalError).
+// rho_io (optional): warm start for the Newton root-find, updated with the
+// root found -- consecutive PDHG trials project nearby points, so Newton
+// starts next to its root instead of at the bracket midpoint.
+__device__ inline void proj_exp3(double r, double s, double t, double* o, int* err,
+                                 double* rho_io = nullptr, RootCfg rc = RootCfg()) {
+  ExpHeur H;
+  if (exp_cheap(r, s, t, o, err, H)) return;
+  if (rho_io && exp_warm(r, s, t, H, o, rho_io)) return;
+  exp_rooted(r, s, t, H, o, rho_io, rc);
+}
+
+// proj_exp3 without the root stage: true when the cheap cases or the warm
+// start decide (o set, *rho_io updated), false when the bracket + root search
+// is needed (o and *rho_io then undefined / untouched).
+__device__ __forceinline__ bool proj_exp3_fast(double r, double s, double t, double* o, int* err,
+                                               double* rho_io) {
+  ExpHeur H;
+  if (exp_cheap(r, s, t, o, err, H)) return true;
+  return exp_warm(r, s, t, H, o, rho_io);
 }
 
 // Dual cone via Moreau: P_{K*}(v) = v + P_K(-v) (cones.py:329-331).
 __device__ inline void proj_dual_exp3(double r, double s, double t, double* o, int* err,
-                                      double* rho_io = nullptr) {
+                                      double* rho_io = nullptr, RootCfg rc = RootCfg()) {
   double q[3];
-  proj_exp3(-r, -s, -t, q, err, rho_io);
+  proj_exp3(-r, -s, -t, q, err, rho_io, rc);
   o[0] = r + q[0]; o[1] = s + q[1]; o[2] = t + q[2];
+}
+
+__device__ __forceinline__ bool proj_dual_exp3_fast(double r, double s, double t, double* o, int* err,
+                                                    double* rho_io) {
+  double q[3];
+  if (!proj_exp3_fast(-r, -s, -t, q, err, rho_io)) return false;
+  o[0] = r + q[0]; o[1] = s + q[1]; o[2] = t + q[2];
+  return true;
 }
 
 __device__ inline void set_err(int* gerr, int code) {
@@ -482,7 +547,8 @@ __device__ inline double rsoc_phi(const G& g, const double* in, const double* sc
 
 template <class G>
 __device__ inline void proj_rescaled_soc(const G& g, const double* in, double* out,
-                                         const double* sc, int smode, int dim, int* gerr) {
+                                         const double* sc, int smode, int dim, int* gerr,
+                                         RootCfg rc = RootCfg()) {
   double d0 = smode == PDCS_SCALE_INVERT ? 1.0 / sc[0] : sc[0];
   double t0 = in[0];
   // membership tests (cones.py:372-375)
@@ -553,17 +619,20 @@ __device__ inline void proj_rescaled_soc(const G& g, const double* in, double* o
     for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
     return;
   }
-  // Brent's method with xtol = 1e-16, rtol = 8.9e-16, 100 iterations
-  // (the classic algorithm scipy's brentq implements).
+  // Brent's method with xtol = 1e-16, rtol = 8.9e-16, maxiter = max_root_iters
+  // (the classic algorithm scipy's brentq implements; not converging within
+  // maxiter raises in scipy, so it is a numerical error here, cones.py:414-425).
   const double xtol = 1e-16, rtol = 8.9e-16;
   double xpre = lo, xcur = hi, xblk = 0.0, fblk = 0.0, spre = 0.0, scur = 0.0;
   double fpre = rsoc_phi(g, in, sc, smode, dim, d0, xpre, t0);
   double fcur = rsoc_phi(g, in, sc, smode, dim, d0, xcur, t0);
   double mu = xcur;
+  bool conv = true;
   if (fpre == 0.0) {
     mu = xpre;
   } else if (fcur != 0.0) {
-    for (int it = 0; it < 100; ++it) {
+    conv = false;
+    for (int it = 0; it < rc.iters; ++it) {
       if (fpre != 0.0 && fcur != 0.0 && (signbit(fpre) != signbit(fcur))) {
         xblk = xpre; fblk = fpre; spre = scur = xcur - xpre;
       }
@@ -573,7 +642,7 @@ __device__ inline void proj_rescaled_soc(const G& g, const double* in, double* o
       }
       double delta = (xtol + rtol * fabs(xcur)) / 2.0;
       double sbis = (xblk - xcur) / 2.0;
-      if (fcur == 0.0 || fabs(sbis) < delta) break;
+      if (fcur == 0.0 || fabs(sbis) < delta) { conv = true; break; }
       if (fabs(spre) > delta && fabs(fcur) < fabs(fpre)) {
         double stry;
         if (xpre == xblk) {
@@ -598,6 +667,7 @@ __device__ inline void proj_rescaled_soc(const G& g, const double* in, double* o
     }
     mu = xcur;
   }
+  if (!conv && g.rank == 0) set_err(gerr, PDCS_ERR_RSOC_ROOT);
   g.sync();
   for (int i = 1 + g.rank; i < dim; i += g.size) {
     double di = smode == PDCS_SCALE_INVERT ? 1.0 / sc[i] : sc[i];
@@ -609,7 +679,8 @@ __device__ inline void proj_rescaled_soc(const G& g, const double* in, double* o
 
 template <class G>
 __device__ inline void proj_segment(const G& g, int kind, int smode, const double* in,
-                                    double* out, const double* sc, int dim, int* gerr) {
+                                    double* out, const double* sc, int dim, int* gerr,
+                                    RootCfg rc = RootCfg()) {
   switch (kind) {
     case PDCS_FREE:
       for (int i = g.rank; i < dim; i += g.size) out[i] = in[i];
@@ -625,8 +696,8 @@ __device__ inline void proj_segment(const G& g, int kind, int smode, const doubl
       if (g.rank == 0) {
         double o[3];
         int e = 0;
-        if (kind == PDCS_EXP) proj_exp3(in[0], in[1], in[2], o, &e);
-        else proj_dual_exp3(in[0], in[1], in[2], o, &e);
+        if (kind == PDCS_EXP) proj_exp3(in[0], in[1], in[2], o, &e, nullptr, rc);
+        else proj_dual_exp3(in[0], in[1], in[2], o, &e, nullptr, rc);
         set_err(gerr, e);
         out[0] = o[0]; out[1] = o[1]; out[2] = o[2];
       }
@@ -642,7 +713,7 @@ __device__ inline void proj_segment(const G& g, int kind, int smode, const doubl
         uniform = g.all(u);
       }
       if (!uniform) {
-        proj_rescaled_soc(g, in, out, sc, smode, dim, gerr);
+        proj_rescaled_soc(g, in, out, sc, smode, dim, gerr, rc);
         g.sync();
         return;
       }

@@ -97,9 +97,10 @@ bool nccl_load() {
     }                                                                                 \
   } while (0)
 
-int nccl_allreduce(const double* send, double* recv, size_t count, void* comm, cudaStream_t s) {
+int nccl_allreduce(const double* send, double* recv, size_t count, void* comm, cudaStream_t s,
+                   ncclRedOp_t op = ncclSum) {
   if (count == 0) return 0;
-  CKN(g_nccl.allReduce(send, recv, count, ncclDouble, ncclSum, (ncclComm_t)comm, s));
+  CKN(g_nccl.allReduce(send, recv, count, ncclDouble, op, (ncclComm_t)comm, s));
   return 0;
 }
 
@@ -373,6 +374,8 @@ int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bo
 }
 
 void free_table(BlockTable& T) {
+  cudaFree(T.d_queue);
+  cudaFree(T.d_qcount);
   cudaFree(T.d_all);
   cudaFree(T.d_gpart);
   cudaFree(T.d_gcoef);
@@ -384,7 +387,15 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
                   int slot0, int gate, cudaStream_t s) {
   int slot = slot0;
   const PdcsBlock* base = T.d_all;
-  if (T.n_exp) {
+  if (T.n_exp && OP == OP_STEP_Y && T.exp_split) {
+    auto fast = T.exp_minb == 2 ? k_exp_y_fast<2> : (T.exp_minb == 3 ? k_exp_y_fast<3> : k_exp_y_fast<4>);
+    fast<<<T.g_exp, BS, 0, s>>>(base, T.n_exp, T.exp_per, A, T.d_queue, T.d_qcount, part, cap, slot, gate);
+    CKL();
+    k_exp_y_slow<<<T.g_exp, BS, 0, s>>>(base, T.exp_per, A, T.d_queue, T.d_qcount, part, cap,
+                                        slot + T.g_exp, gate);
+    CKL();
+    slot += T.g_exp;
+  } else if (T.n_exp) {
     k_blk_exp<OP><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
     CKL();
   }
@@ -854,7 +865,18 @@ int pdcs_transpose_csr(int32_t nrows, int32_t ncols, int32_t nnz, const int32_t*
 
 int pdcs_project_segments(int32_t len, const double* d_in, double* d_out, const PdcsBlock* h_blocks,
                           int32_t nblocks, const double* d_scale, int32_t* h_err, void* stream) {
+  return pdcs_project_segments_ex(len, d_in, d_out, h_blocks, nblocks, d_scale, 1e-12, 100, h_err,
+                                  stream);
+}
+
+int pdcs_project_segments_ex(int32_t len, const double* d_in, double* d_out, const PdcsBlock* h_blocks,
+                             int32_t nblocks, const double* d_scale, double root_tol,
+                             int32_t max_root_iters, int32_t* h_err, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (!(root_tol >= 0.0) || max_root_iters < 1) {
+    g_err = "pdcs_project_segments_ex: root_tol must be >= 0 and max_root_iters >= 1";
+    return 2;
+  }
   if (len < 0 || nblocks < 0) { g_err = "pdcs_project_segments: bad sizes"; return 2; }
   for (int i = 0; i < nblocks; ++i) {
     const PdcsBlock& b = h_blocks[i];
@@ -878,6 +900,8 @@ int pdcs_project_segments(int32_t len, const double* d_in, double* d_out, const 
   std::memset(&A, 0, sizeof(A));
   A.err = d_err;
   BlkParams P{d_out, d_out, d_scale, 0, -1};
+  P.rc.tol = root_tol;
+  P.rc.iters = max_root_iters;
   int rc = launch_blocks<OP_PROJECT>(T, A, P, nullptr, 0, 0, 0, s);
   int herr = 0;
   CK(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -938,6 +962,21 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   if (E->tabY.n_exp) {  // Newton warm starts of the dual exp blocks, NaN = cold
     const size_t cnt = 2 * (size_t)E->tabY.n_exp;
     if (cudaMalloc(&E->d_exp_rho, sizeof(double) * cnt) != cudaSuccess) return fail(1);
+    // fast / slow split of the y-step exp blocks (PDCS_TUNE=expsplit=1).  Off by
+    // default: measured slower on C3 (blocks_y 0.146-0.172 ms vs 0.135 ms in
+    // one kernel, 2.27-2.41k vs 2.75k it/s; profiles/r02_sweeps.txt)
+    const char* env = getenv("PDCS_TUNE");
+    const bool on = env && (strstr(env, "expsplit=1") != nullptr);
+    if (on) {
+      BlockTable& T = E->tabY;
+      T.exp_split = true;
+      const char* mb = env ? strstr(env, "expminb=") : nullptr;
+      if (mb) T.exp_minb = atoi(mb + 8);
+      T.exp_per = (T.n_exp + T.g_exp - 1) / T.g_exp;
+      if (cudaMalloc(&T.d_queue, sizeof(int) * T.n_exp) != cudaSuccess ||
+          cudaMalloc(&T.d_qcount, sizeof(int) * T.g_exp) != cudaSuccess)
+        return fail(1);
+    }
     std::vector<double> nan_init(cnt, NAN);
     if (cudaMemcpyAsync(E->d_exp_rho, nan_init.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice,
                         s) != cudaSuccess ||
@@ -1148,14 +1187,21 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
     k_fill<<<grid_for(n), BS, 0, s>>>(d.d_d2, n, 1.0);
     CKL();
   }
-  if (enabled == 1 && nnz > 0) {
+  // sharded engine (communicator attached): this rank holds a row slice of
+  // G; row statistics are local, column statistics are all-reduced over the
+  // ranks (max-abs for Ruiz, sums of |a_ij| for Pock-Chambolle), so every
+  // rank ends with its slice of D1 and the global D2 (SURVEY 8(e) "At setup")
+  const bool shard = E->comm && E->nranks > 1;
+  if (enabled == 1 && (nnz > 0 || shard)) {
     // Ruiz rounds on a working copy held in g_val (scaling.py:84-90)
-    CK(cudaMemcpyAsync(d.d_g_val, d.d_g_val0, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    if (nnz > 0)
+      CK(cudaMemcpyAsync(d.d_g_val, d.d_g_val0, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
     for (int it = 0; it < ruiz_iters; ++it) {
       k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
       CKL();
       if (launch_rowred<0>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
       if (launch_rowred<0>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
+      if (shard && nccl_allreduce(d.d_tx0, d.d_tx0, n, E->comm, s, ncclMax)) return 1;
       k_inv_sqrt_mul<<<grid_for(m), BS, 0, s>>>(d.d_ty0, d.d_ty1, d.d_d1, m);
       CKL();
       k_inv_sqrt_mul<<<grid_for(n), BS, 0, s>>>(d.d_tx0, d.d_tx1, d.d_d2, n);
@@ -1169,6 +1215,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
       CKL();
       if (launch_rowred<1>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
       if (launch_rowred<1>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
+      if (shard && nccl_allreduce(d.d_tx0, d.d_tx0, n, E->comm, s, ncclSum)) return 1;
       k_inv_sqrt_mul<<<grid_for(m), BS, 0, s>>>(d.d_ty0, d.d_ty1, d.d_d1, m);
       CKL();
       k_inv_sqrt_mul<<<grid_for(n), BS, 0, s>>>(d.d_tx0, d.d_tx1, d.d_d2, n);
@@ -1363,10 +1410,11 @@ int pdcs_engine_spmv(PdcsEngine* E, int32_t transpose, const double* in, double*
 }
 
 static int project_blocks(Engine* E, const BlockTable& T, const double* buf, int dualize, int smode,
-                          const double* scale) {
+                          const double* scale, RootCfg rcfg = RootCfg()) {
   if (T.total() == 0) return 0;
   const KArgs A = make_args(E);
   BlkParams P{buf, const_cast<double*>(buf), scale, dualize, smode};
+  P.rc = rcfg;
   return launch_blocks<OP_PROJECT>(T, A, P, nullptr, 0, 0, 0, E->stream);
 }
 
@@ -1510,19 +1558,31 @@ int pdcs_dot_diff(PdcsEngine* E, int32_t space, const double* a, const double* b
 }
 
 int pdcs_project_set(PdcsEngine* E, int32_t which, const double* in, double* out) {
+  return pdcs_project_set_ex(E, which, in, out, 1e-12, 100);
+}
+
+int pdcs_project_set_ex(PdcsEngine* E, int32_t which, const double* in, double* out, double root_tol,
+                        int32_t max_root_iters) {
   const KArgs A = make_args(E);
   cudaStream_t s = E->stream;
   if (which < 0 || which > 4) { g_err = "pdcs_project_set: bad set"; return 2; }
+  if (!(root_tol >= 0.0) || max_root_iters < 1) {
+    g_err = "pdcs_project_set_ex: root_tol must be >= 0 and max_root_iters >= 1";
+    return 2;
+  }
+  RootCfg rcfg;
+  rcfg.tol = root_tol;
+  rcfg.iters = max_root_iters;
   const bool xs = which == 0 || which == 3 || which == 4;
   k_proj_elem<<<xs ? E->gridX : E->gridY, BS, 0, s>>>(A, which, in, out);
   CKL();
   int rc = 0;
   switch (which) {
-    case 0: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2); break;
-    case 1: rc = project_blocks(E, E->tabY, out, 1, PDCS_SCALE_DIRECT, E->d.d_d1); break;
-    case 2: rc = project_blocks(E, E->tabY, out, 0, PDCS_SCALE_INVERT, E->d.d_d1); break;
-    case 3: rc = project_blocks(E, E->tabX, out, 1, PDCS_SCALE_INVERT, E->d.d_d2); break;
-    case 4: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2); break;
+    case 0: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2, rcfg); break;
+    case 1: rc = project_blocks(E, E->tabY, out, 1, PDCS_SCALE_DIRECT, E->d.d_d1, rcfg); break;
+    case 2: rc = project_blocks(E, E->tabY, out, 0, PDCS_SCALE_INVERT, E->d.d_d1, rcfg); break;
+    case 3: rc = project_blocks(E, E->tabX, out, 1, PDCS_SCALE_INVERT, E->d.d_d2, rcfg); break;
+    case 4: rc = project_blocks(E, E->tabX, out, 0, PDCS_SCALE_DIRECT, E->d.d_d2, rcfg); break;
   }
   if (rc) return rc;
   return check_err(E);

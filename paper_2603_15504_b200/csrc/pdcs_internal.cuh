@@ -58,8 +58,18 @@ struct BlockTable {
   int g_exp = 0, g_thread = 0, g_half = 0, g_warp = 0, g_cta = 0, g_giant = 0;  // fixed grids (partial slots)
   double* d_gpart = nullptr;  // giant-block partial sums [n_giant][2][g_giant]
   double* d_gcoef = nullptr;  // giant-block SOC coefficients [n_giant][8]
+  // y-step exp blocks in two launches (k_exp_y_fast / k_exp_y_slow): CTA c of
+  // the fast kernel owns blocks [c*exp_per, (c+1)*exp_per) and queues the ones
+  // needing the root search at d_queue[c*exp_per ...], d_qcount[c] of them
+  bool exp_split = false;
+  int exp_per = 0;
+  int exp_minb = 2;  // CTAs per SM the fast kernel is compiled for (register budget)
+  int* d_queue = nullptr;   // [n_exp]
+  int* d_qcount = nullptr;  // [g_exp]
   int total() const { return n_exp + n_thread + n_half + n_warp + n_cta + n_giant; }
-  int grids() const { return g_exp + g_thread + g_half + g_warp + g_cta + g_giant; }
+  int grids() const {
+    return g_exp * (exp_split ? 2 : 1) + g_thread + g_half + g_warp + g_cta + g_giant;
+  }
 };
 
 constexpr int GIANT_MIN = 1 << 16;  // uniform dual SOC blocks above this use the whole grid

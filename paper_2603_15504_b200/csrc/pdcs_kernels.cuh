@@ -418,6 +418,7 @@ struct BlkParams {
   const double* scale;
   int dualize;
   int smode;  // -1: use the block's own smode
+  RootCfg rc;  // ProjectionSettings of the standalone projection API
 };
 
 struct ThreadGrp {
@@ -435,7 +436,7 @@ __device__ __forceinline__ void do_block(const Grp& g, const PdcsBlock& b, const
   if (OP == OP_PROJECT) {
     const int kind = P.dualize ? dual_kind(b.kind) : b.kind;
     const int sm = P.smode >= 0 ? P.smode : b.smode;
-    proj_segment(g, kind, sm, P.in + s, P.out + s, sm ? P.scale + s : nullptr, dim, A.err);
+    proj_segment(g, kind, sm, P.in + s, P.out + s, sm ? P.scale + s : nullptr, dim, A.err, P.rc);
     g.sync();
   } else if (OP == OP_STEP_X) {
     proj_segment(g, b.kind, PDCS_SCALE_DIRECT, A.xh + s, A.xh + s, A.d2 + s, dim, A.err);
@@ -483,9 +484,15 @@ __device__ __forceinline__ void do_block(const Grp& g, const PdcsBlock& b, const
 // Exponential-cone blocks (always 3-dimensional, block-uniform scale): one
 // thread per block with straight-line code, no generic segment machinery.
 __device__ __forceinline__ void exp_or_dual(int kind, const double* v, double* o, int* err,
-                                            double* rho = nullptr) {
-  if (kind == PDCS_EXP) proj_exp3(v[0], v[1], v[2], o, err, rho);
-  else proj_dual_exp3(v[0], v[1], v[2], o, err, rho);
+                                            double* rho = nullptr, RootCfg rc = RootCfg()) {
+  if (kind == PDCS_EXP) proj_exp3(v[0], v[1], v[2], o, err, rho, rc);
+  else proj_dual_exp3(v[0], v[1], v[2], o, err, rho, rc);
+}
+
+__device__ __forceinline__ bool exp_or_dual_fast(int kind, const double* v, double* o, int* err,
+                                                 double* rho) {
+  if (kind == PDCS_EXP) return proj_exp3_fast(v[0], v[1], v[2], o, err, rho);
+  return proj_dual_exp3_fast(v[0], v[1], v[2], o, err, rho);
 }
 
 template <int OP>
@@ -503,7 +510,7 @@ __global__ void __launch_bounds__(BS, 4) k_blk_exp(const PdcsBlock* tab, int nb,
     double v[3], o[3];
     if (OP == OP_PROJECT) {
       for (int q = 0; q < 3; ++q) v[q] = P.in[s + q];
-      exp_or_dual(P.dualize ? dual_kind(b.kind) : b.kind, v, o, &err);
+      exp_or_dual(P.dualize ? dual_kind(b.kind) : b.kind, v, o, &err, nullptr, P.rc);
       for (int q = 0; q < 3; ++q) P.out[s + q] = o[q];
     } else if (OP == OP_STEP_X) {
       for (int q = 0; q < 3; ++q) v[q] = A.xh[s + q];
@@ -548,6 +555,117 @@ __global__ void __launch_bounds__(BS, 4) k_blk_exp(const PdcsBlock* tab, int nb,
   }
   if (err) set_err(A.err, err);
   if (OP != OP_PROJECT) block_store_mask<NQ>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
+// Exponential-cone blocks of the y-step in two launches (C3: 1M blocks).  In
+// one thread-per-block kernel the warps of the common case -- cheap cases
+// and the warm-started Newton -- wait for the few lanes whose blocks need the
+// reference's bracket + safeguarded Newton + bisection (up to 100 h
+// evaluations).  So:
+//  (1) k_exp_y_fast: CTA c owns blocks [c*per, (c+1)*per).  A block whose two
+//      projections (y_hat onto the dual kind, the residual onto the kind)
+//      are both decided by the fast path is finished here; otherwise nothing
+//      of it is written and its index is queued, in block order, in CTA c's
+//      queue (warp ballots + a CTA prefix: deterministic).
+//  (2) k_exp_y_slow: CTA c runs the full projections of its queue -- exactly
+//      the computation k_blk_exp<OP_STEP_Y> does for those blocks.
+// Each block's result is the single-kernel result bit for bit; the line-search
+// sums are per-CTA partials in fixed slots (deterministic).
+__device__ __forceinline__ void exp_y_finish(const KArgs& A, int s, const double* o,
+                                             const double* res, const double* rp, double* acc) {
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int r = s + q;
+    const double yn = A.y[r], p = o[q], hi = A.h[r];
+    A.yh[r] = p;
+    const double dy = p - yn;
+    acc[GY_YY] += yn * yn;
+    acc[GY_DYDY] += dy * dy;
+    acc[GY_INTER] += dy * (A.w[r] - A.gx[r]);
+    const double viol = res[q] - rp[q];
+    acc[GY_RP2] += viol * viol;
+    acc[GY_YH] += p * hi;
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_exp_y_fast(const PdcsBlock* tab, int nb, int per, KArgs A,
+                                                   int* queue, int* qcount, double* part, int cap,
+                                                   int slot0, int gate) {
+  if (gated(A.ctrl, gate)) return;
+  __shared__ int wcnt[BS / 32];
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  int err = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int b0 = blockIdx.x * per, b1 = min(nb, b0 + per);
+  int qn = 0;
+  for (int c = b0; c < b1; c += BS) {
+    const int i = c + threadIdx.x;
+    bool miss = false;
+    if (i < b1) {
+      const PdcsBlock b = tab[i];
+      const int s = b.start;
+      double v[3], o[3], res[3], rp[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        v[q] = A.yh[s + q];
+        res[q] = A.gxh[s + q] - A.h[s + q];
+      }
+      double rho0 = A.exp_rho[2 * (size_t)i], rho1 = A.exp_rho[2 * (size_t)i + 1];
+      int e = 0;
+      const bool ok = exp_or_dual_fast(dual_kind(b.kind), v, o, &e, &rho0) &&
+                      exp_or_dual_fast(b.kind, res, rp, &e, &rho1);
+      if (ok) {
+        A.exp_rho[2 * (size_t)i] = rho0;
+        A.exp_rho[2 * (size_t)i + 1] = rho1;
+        exp_y_finish(A, s, o, res, rp, acc);
+        err |= e;
+      } else {
+        miss = true;
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, miss);
+    if (lane == 0) wcnt[wid] = __popc(bal);
+    __syncthreads();
+    int off = qn, tot = 0;
+#pragma unroll
+    for (int w = 0; w < BS / 32; ++w) {
+      const int cw = wcnt[w];
+      if (w < wid) off += cw;
+      tot += cw;
+    }
+    if (miss) queue[b0 + off + __popc(bal & ((1u << lane) - 1u))] = i;
+    qn += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) qcount[blockIdx.x] = qn;
+  if (err) set_err(A.err, err);
+  block_store_mask<GY_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
+__global__ void __launch_bounds__(BS, 2) k_exp_y_slow(const PdcsBlock* tab, int per, KArgs A,
+                                                   const int* queue, const int* qcount, double* part,
+                                                   int cap, int slot0, int gate) {
+  if (gated(A.ctrl, gate)) return;
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  int err = 0;
+  const int cnt = qcount[blockIdx.x];
+  for (int k = threadIdx.x; k < cnt; k += BS) {
+    const int i = queue[blockIdx.x * per + k];
+    const PdcsBlock b = tab[i];
+    const int s = b.start;
+    double v[3], o[3], res[3], rp[3];
+    for (int q = 0; q < 3; ++q) {
+      v[q] = A.yh[s + q];
+      res[q] = A.gxh[s + q] - A.h[s + q];
+    }
+    double* rho = A.exp_rho + 2 * (size_t)i;
+    exp_or_dual(dual_kind(b.kind), v, o, &err, rho);
+    exp_or_dual(b.kind, res, rp, &err, rho + 1);
+    exp_y_finish(A, s, o, res, rp, acc);
+  }
+  if (err) set_err(A.err, err);
+  block_store_mask<GY_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }
 
 template <int OP>

@@ -7,6 +7,7 @@ all arithmetic runs in libpdcs kernels (include/pdcs.h).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -61,16 +62,20 @@ def _slab(dtype, sizes: dict, align: int = 64) -> dict:
 
 
 _STAGE_BYTES = 32 << 20
-_stage_bufs = None
+_stage_local = threading.local()
 
 
 def _stages():
-    """Two reusable pinned host buffers for double-buffered transfers."""
-    global _stage_bufs
-    if _stage_bufs is None:
+    """Two reusable pinned host buffers for double-buffered transfers, one
+    pair per host thread: `solve_many` runs concurrent solves on several
+    threads, and a shared pair would let one thread overwrite a chunk another
+    thread's async copy is still reading."""
+    bufs = getattr(_stage_local, "bufs", None)
+    if bufs is None:
         torch = _torch()
-        _stage_bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-    return _stage_bufs
+        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        _stage_local.bufs = bufs
+    return bufs
 
 
 def h2d(dst, arr, stream) -> None:
@@ -179,10 +184,12 @@ class DeviceCSR:
         return self._apply(self.n, self.trp, self.tci, self.tva, y)
 
 
-def project_segments(v: np.ndarray, blocks, scale: np.ndarray | None = None) -> np.ndarray:
+def project_segments(v: np.ndarray, blocks, scale: np.ndarray | None = None,
+                     root_tol: float = 1e-12, max_root_iters: int = 100) -> np.ndarray:
     """Segmented cone projection of a host vector on the GPU.
 
-    blocks: iterable of (kind_code, start, dim, smode).  Returns (out, err)."""
+    blocks: iterable of (kind_code, start, dim, smode); root_tol /
+    max_root_iters: the ProjectionSettings fields.  Returns (out, err)."""
     lib = N.lib()
     v = np.ascontiguousarray(v, dtype=np.float64)
     blocks = list(blocks)
@@ -193,8 +200,9 @@ def project_segments(v: np.ndarray, blocks, scale: np.ndarray | None = None) -> 
     dout = _empty_f64(v.size)
     dsc = _dev_f64(scale) if scale is not None else None
     err = C.c_int32(0)
-    N.check(lib.pdcs_project_segments(v.size, _ptr(din), _ptr(dout), arr, len(blocks), _ptr(dsc),
-                                      C.byref(err), None), "pdcs_project_segments")
+    N.check(lib.pdcs_project_segments_ex(v.size, _ptr(din), _ptr(dout), arr, len(blocks), _ptr(dsc),
+                                         float(root_tol), int(max_root_iters), C.byref(err), None),
+            "pdcs_project_segments_ex")
     return dout[: v.size].cpu().numpy(), int(err.value)
 
 
@@ -412,8 +420,9 @@ class DeviceEngine:
                 "pdcs_dot_diff")
         return float(out[0])
 
-    def project_set(self, which: int, src, dst):
-        rc = self.lib.pdcs_project_set(self.handle, int(which), _ptr(src), _ptr(dst))
+    def project_set(self, which: int, src, dst, root_tol: float = 1e-12, max_root_iters: int = 100):
+        rc = self.lib.pdcs_project_set_ex(self.handle, int(which), _ptr(src), _ptr(dst), float(root_tol),
+                                          int(max_root_iters))
         if rc == 3:
             from .linalg import NumericalError
 

@@ -17,9 +17,10 @@ state, after which every rank holds identical full copies; the check path
 then runs the reference's host logic on reductions that `ShardedDevice`
 combines across ranks with torch.distributed.
 
-Preconditioning: every rank computes the Ruiz + Pock-Chambolle scaling of the
-FULL matrix on its GPU (exactly the single-GPU scaling), keeps its slice of D1
-and all of D2, then drops the full copy.
+Preconditioning: each rank uploads only its row slice; Ruiz + Pock-Chambolle
+runs on the slice with the column statistics (max-abs per Ruiz round, 1-norms
+for Pock-Chambolle) all-reduced over the ranks inside libpdcs, so every rank
+holds its slice of D1 and the global D2 (SURVEY.md 8(e) "At setup").
 """
 
 from __future__ import annotations
@@ -171,6 +172,18 @@ def torch_allreduce(group=None):
     return run
 
 
+def combine_stats(stats: dict, allreduce) -> dict:
+    """A rank's pdcs_stats over its row slice -> the whole instance's: the
+    y-space norms of h add, the matrix maxima (max |G^_ij|, max row 1-norm)
+    take the max, the x-space norms of c are already global."""
+    out = dict(stats)
+    s = allreduce(np.array([stats["h1"], stats["h2"]]), "sum")
+    mx = allreduce(np.array([stats["gmax"], stats["rowsum_max"]]), "max")
+    out["h1"], out["h2"] = float(s[0]), float(s[1])
+    out["gmax"], out["rowsum_max"] = float(mx[0]), float(mx[1])
+    return out
+
+
 class ShardedDevice:
     """A rank's DeviceEngine whose reductions and G^T products are combined
     across ranks, so the single-GPU `_Loop` host logic runs unchanged."""
@@ -243,48 +256,44 @@ def _make_sharded_loop_class():
             super().__init__(original, options)
 
         def _make_device(self, options):
+            import ctypes
+
             import torch
             import torch.distributed as dist
 
             work = self.work
             enabled = 1 if (options.use_preconditioner and work.G.nnz > 0) else 0
-            full = DeviceEngine(work, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc,
-                                x_pad=self._world)
-            full.precondition(enabled, options.ruiz_iterations, options.use_pock_chambolle)
-            stats = full.stats()
             r0, r1 = partition_rows(work, self._world)[self._rank]
             self.row_range = (r0, r1)
             local = slice_problem(work, r0, r1)
+            # only the rank's row slice is uploaded (and transposed, and panelled)
             dev = DeviceEngine(local, allow_nonuniform_dual_soc=options.allow_nonuniform_dual_soc,
                                x_pad=self._world)
-            with torch.cuda.stream(dev.stream):
-                if r1 > r0:
-                    dev.d1[: r1 - r0].copy_(full.d1[r0:r1])
-                dev.d2[: work.n].copy_(full.d2[: work.n])
-            dev.stream.synchronize()
-            dev.precondition(3)
-            del full
-            torch.cuda.empty_cache()
-            # NCCL communicator of libpdcs (its collectives live in the graph)
+            # NCCL communicator of libpdcs (its collectives live in the graph and
+            # in the sharded preconditioning)
             buf = [None]
             if self._rank == 0:
-                import ctypes
-
                 idb = ctypes.create_string_buffer(128)
                 N.check(dev.lib.pdcs_comm_unique_id(idb), "pdcs_comm_unique_id")
                 buf = [bytes(idb.raw)]
             dist.broadcast_object_list(buf, src=0, group=self._group)
             N.check(dev.lib.pdcs_engine_set_comm(dev.handle, buf[0], self._rank, self._world),
                     "pdcs_engine_set_comm")
-            import ctypes
-
             self.xcuts = partition_cols(work, self._world)
             cuts = (ctypes.c_int32 * len(self.xcuts))(*self.xcuts)
             N.check(dev.lib.pdcs_engine_set_xsplit(dev.handle, cuts, self._world), "pdcs_engine_set_xsplit")
+            # Ruiz + Pock-Chambolle on the slice: row statistics local, column
+            # statistics all-reduced inside libpdcs (max / sum over the ranks)
+            dev.precondition(enabled, options.ruiz_iterations, options.use_pock_chambolle)
             ar = torch_allreduce(self._group)
+            stats = combine_stats(dev.stats(), ar)
 
             def vec_ar(t):
-                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self._group)
+                # the engine stream is the current stream, so NCCL orders the
+                # all-reduce after the engine's kernels that wrote `t` and the
+                # engine's next kernels (metrics, rays, gap probes) after it
+                with torch.cuda.stream(dev.stream):
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self._group)
 
             self.local_problem = local
             return ShardedDevice(dev, ar, vec_ar, work.m), stats

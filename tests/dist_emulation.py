@@ -19,7 +19,66 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
 
-def sharded_run(rank, world, make_problem, iters, port, out_path):
+def _gap_dist(x, y, b1, b2, r, tau, sigma, px, py, xdot, ydot, t0=1.0, eps_rel=1e-8):
+    """The oracle's normalized_gap (S/restart.py:80-132) with every dot
+    product combined across the ranks: x-space dots over the rank's x-slice,
+    y-space dots over its rows, both all-reduced (the check-path reductions
+    ShardedDevice combines on GPUs).  Same probe sequence and stopping rules."""
+    from oracle import pdcs_oracle as O
+
+    if r <= O.GAP_TINY_R:
+        return 0.0
+
+    def zt(t):
+        return px(x + (t * tau) * b1), py(y + (t * sigma) * b2)
+
+    def dist(zx, zy):
+        dx, dy = x - zx, y - zy
+        return math.sqrt(xdot(dx, dx) / tau + ydot(dy, dy) / sigma)
+
+    def value(zx, zy):
+        return (xdot(b1, zx - x) + ydot(b2, zy - y)) / r
+
+    tl, tr = 0.0, t0
+    tk = t0
+    zx, zy = zt(tk)
+    d = dist(zx, zy)
+    if not d > r:
+        prev, stalls, found = d, 0, False
+        for _ in range(O.GAP_MAX_DOUBLE):
+            tk *= 2.0
+            zx, zy = zt(tk)
+            d = dist(zx, zy)
+            if d > r:
+                tr, tl, found = tk, tk / 2.0, True
+                break
+            if d <= prev * (1.0 + 1e-13):
+                stalls += 1
+                if stalls >= 2:
+                    return value(zx, zy)
+            else:
+                stalls = 0
+            prev = d
+        if not found:
+            raise O.OracleGapError("no bracket")
+    eps = eps_rel * max(1.0, tr)
+    zx, zy = zt(0.5 * (tl + tr))
+    while tr - tl > eps:
+        tm = 0.5 * (tl + tr)
+        zx, zy = zt(tm)
+        d = dist(zx, zy)
+        if d < r:
+            tl = tm
+        else:
+            tr = tm
+    return value(zx, zy)
+
+
+def sharded_run(rank, world, make_problem, iters, port, out_path, restart_freq=None):
+    """restart_freq: None = restarts off; else duality-gap restarts checked
+    every restart_freq k_bar (products refreshed, candidate z vs z_bar by the
+    cross-rank normalized gap, restart criteria and primal-weight update of
+    S/engine.py:467-544, S/restart.py:148-211)."""
     import torch
     import torch.distributed as dist
 
@@ -47,15 +106,15 @@ def sharded_run(rank, world, make_problem, iters, port, out_path):
     omega = nc / nh if (nc > 1e-10 and nh > 1e-10) else 1.0
     h1, c1 = float(np.sum(np.abs(full.h))), float(np.sum(np.abs(full.c)))
 
-    # x-split: this rank steps x-slice [c0, c1); outside it the x-space state
+    # x-split: this rank steps x-slice [xc0, xc1); outside it the x-space state
     # is poisoned with NaN, so any use of another rank's entries shows up in
     # the result.  Exchanged per trial exactly as the sharded CUDA graph does:
     # all-gather of x~, all-reduce of the x- and y-space sums, reduce of the
     # G^T y_hat partials onto the owner's slice.
     cuts = partition_cols(work, world)
-    c0, c1 = cuts[rank], cuts[rank + 1]
+    xc0, xc1 = cuts[rank], cuts[rank + 1]
     own = np.zeros(S.n, dtype=bool)
-    own[c0:c1] = True
+    own[xc0:xc1] = True
 
     def poison(v):
         v = np.array(v, dtype=np.float64)
@@ -64,7 +123,7 @@ def sharded_run(rank, world, make_problem, iters, port, out_path):
 
     def allgather_x(v):
         parts = [None] * world
-        dist.all_gather_object(parts, v[c0:c1])
+        dist.all_gather_object(parts, v[xc0:xc1])
         return np.concatenate(parts)
 
     def xdot(a, b):  # x-space sum over the slice, then over the ranks
@@ -74,12 +133,42 @@ def sharded_run(rank, world, make_problem, iters, port, out_path):
     bown = own[:nbox]
     x, y = poison(np.zeros(S.n)), np.zeros(S.m)
     xa, ya = x.copy(), y.copy()
+    xpa = ypa = None
     xb = yb = None
     W = 0.0
     gx, gty = S.mv(np.zeros(S.n)), poison(ar(S.rmv(y)))
     gxa, gtya = gx.copy(), gty.copy()
     k = k_bar = 0
     lf, uf = np.isfinite(S.l), np.isfinite(S.u)
+
+    def ydot(a, b):
+        return float(ar(np.dot(a, b))[0])
+
+    def px(v):
+        return poison(O.proj_X(S, np.where(own, v, 0.0)))
+
+    def py(v):
+        return O.proj_Y(S, v)
+
+    def products(xv, yv):  # G^ x (local rows, x all-gathered) and G^T y (reduced onto owners)
+        return S.mv(allgather_x(xv)), poison(ar(S.rmv(yv)))
+
+    def gap_at(xv, yv, r, om, et):
+        gxv, gtyv = products(xv, yv)
+        return _gap_dist(xv, yv, gtyv - S.c, S.h - gxv, r, et / om, et * om, px, py, xdot, ydot)
+
+    def nnorm(dx, dy, om, et):
+        return math.sqrt(xdot(dx, dx) / (et / om) + ydot(dy, dy) / (et * om))
+
+    omega0 = omega
+    restarts, gap0, prev_cand = 0, None, math.inf
+    if restart_freq:
+        # baseline gap at z0 with the radius of one plain PDHG step at eta_hat (S/engine.py:380-391)
+        tau, sigma = eta_hat / omega, eta_hat * omega
+        xr = px(x - tau * (S.c - gty))
+        w0 = S.mv(allgather_x(2.0 * xr - x))
+        yr = py(y + sigma * (S.h - w0))
+        gap0 = gap_at(x, y, nnorm(x - xr, y - yr, omega, eta_hat), omega, eta_hat)
     for _ in range(iters):
         k_bar += 1
         grad = S.c - gty
@@ -132,10 +221,37 @@ def sharded_run(rank, world, make_problem, iters, port, out_path):
             tot = W + eta_used
             xb, yb, W = (W * xb + eta_used * x) / tot, (W * yb + eta_used * y) / tot, tot
         k += 1
+        if restart_freq and k_bar % restart_freq == 0 and k >= 1:
+            gx, gty = products(x, y)  # product refresh at every check (S/engine.py:631)
+
+            def gm(xv, yv):
+                return gap_at(xv, yv, nnorm(xv - xa, yv - ya, omega, eta_used), omega, eta_used)
+
+            g1, g2 = gm(x, y), gm(xb, yb)
+            (pxk, pyk), val = ((x, y), g1) if g1 <= g2 else ((xb, yb), g2)
+            assert val >= -1e-12 and gap0 >= -1e-12, "KKT-mode fallback is not emulated"
+            fire = (val <= O.R_SUFF * gap0 or (val > prev_cand and val <= O.R_NEC * gap0)
+                    or k >= O.R_ART * k_bar)
+            if not fire:
+                prev_cand = val
+            else:
+                xpa, ypa = xa, ya
+                xa, ya = pxk.copy(), pyk.copy()
+                x, y = pxk.copy(), pyk.copy()
+                dxn, dyn = math.sqrt(xdot(xa - xpa, xa - xpa)), math.sqrt(ydot(ya - ypa, ya - ypa))
+                wn = omega
+                if dxn > 1e-10 and dyn > 1e-10:
+                    wn = math.exp(O.THETA * math.log(dyn / dxn) + (1.0 - O.THETA) * math.log(omega))
+                omega = omega0 if (wn > O.W_MAX or wn < O.W_MIN) else wn
+                restarts += 1
+                k, xb, yb, W, prev_cand, gap0 = 0, None, None, 0.0, math.inf, val
+                gx, gty = products(x, y)
+                gxa, gtya = gx.copy(), gty.copy()
     x = allgather_x(x)
     parts = [None] * world
     dist.all_gather_object(parts, y)
     if rank == 0:
-        np.savez(out_path, x=x, y=np.concatenate(parts), k_bar=k_bar, rows=np.array([r0, r1]))
+        np.savez(out_path, x=x, y=np.concatenate(parts), k_bar=k_bar, rows=np.array([r0, r1]),
+                 restarts=restarts)
     dist.barrier()
     dist.destroy_process_group()

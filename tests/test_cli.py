@@ -51,10 +51,14 @@ def test_invalid_options_are_usage_errors(tmp_path):
 
 def test_threads_env_is_validated(tmp_path, monkeypatch):
     _, path = _write_problem(tmp_path)
+    # reference cli.py:66-78, 86: SystemExit(message) outside the usage-error path
+    # (T/test_cli.py test_threads_env_validation expects pytest.raises(SystemExit))
     monkeypatch.setenv("CONIC_PDHG_THREADS", "zero")
-    assert _main(["--input", str(path)]) == 64
+    with pytest.raises(SystemExit, match="must be an integer"):
+        _main(["--input", str(path)])
     monkeypatch.setenv("CONIC_PDHG_THREADS", "0")
-    assert _main(["--input", str(path)]) == 64
+    with pytest.raises(SystemExit, match="at least 1"):
+        _main(["--input", str(path)])
 
 
 def test_help_exits_zero():

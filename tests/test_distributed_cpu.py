@@ -134,3 +134,32 @@ def test_sharded_iterations_match_single_process_oracle(tmp_path, name, world):
     for key in ("x", "y"):
         scale = max(1.0, float(np.max(np.abs(snap[key]))))
         assert np.max(np.abs(got[key] - snap[key])) <= 1e-9 * scale, key
+
+
+@pytest.mark.parametrize("name,world", [("lp", 2), ("socp", 3), ("exp", 2), ("rsoc", 2), ("prim", 2)])
+def test_sharded_restarts_match_single_process_oracle(tmp_path, name, world):
+    """Restarts on (checks every 10 k_bar): the products are refreshed and the
+    restart candidate is chosen by the normalized duality gap with every dot
+    product combined across the ranks, then the restart criteria and the
+    primal-weight update run on the combined scalars -- the same iterates,
+    k_bar and restart count as the single-process oracle."""
+    iters, freq = 45, 10
+    out = str(tmp_path / "sharded_rs.npz")
+    mp.start_processes(sharded_run, args=(world, PROBLEMS[name], iters, _free_port(), out, freq),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.load(out)
+    kb = int(got["k_bar"])
+    assert kb % freq != 0  # the snapshot below is taken before any check at kb
+    snap = {}
+
+    def cb(st, loop):
+        if st.k_bar == kb:
+            snap["x"], snap["y"], snap["restarts"] = st.x.copy(), st.y.copy(), loop.restarts
+
+    o = O.options_from(None, duality_gap_restart_freq=freq, max_iter=kb, rel_tol=1e-300, abs_tol=1e-300)
+    O.solve(PROBLEMS[name](), o, callback=cb)
+    assert "x" in snap, "the oracle never reached the emulation's k_bar"
+    assert int(got["restarts"]) == snap["restarts"] >= 1, (int(got["restarts"]), snap["restarts"])
+    for key in ("x", "y"):
+        scale = max(1.0, float(np.max(np.abs(snap[key]))))
+        assert np.max(np.abs(got[key] - snap[key])) <= 1e-9 * scale, key

@@ -1,0 +1,325 @@
+// C5 y-step SpMV lab: w = G x~ over a C5-shaped matrix (m = 10M rows of 5
+// uniformly random columns, n = 20M) fused with a 13-vector y-space epilogue,
+// in column panels, with variants of the pass schedule.  Standalone (no
+// libpdcs); each variant is timed with CUDA events after a producer kernel
+// that streams the x-space like k_step_x and writes x~ (so L2 holds what it
+// holds in the real loop).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o c5_lab tools/c5_lab.cu
+//   ./c5_lab [reps]
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                     \
+  do {                                                                            \
+    cudaError_t e_ = (x);                                                         \
+    if (e_ != cudaSuccess) {                                                      \
+      fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
+      exit(1);                                                                    \
+    }                                                                             \
+  } while (0)
+
+constexpr int BS = 256;
+constexpr int M = 10'000'000, N = 20'000'000, K = 5;
+
+__device__ __forceinline__ uint32_t hash32(uint64_t x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+__global__ void k_gen(int* col, double* val) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    int c[K];
+    for (int k = 0; k < K; ++k) c[k] = hash32((uint64_t)r * K + k + 12345) % N;
+    for (int i = 1; i < K; ++i)
+      for (int j = i; j > 0 && c[j - 1] > c[j]; --j) { int t = c[j]; c[j] = c[j - 1]; c[j - 1] = t; }
+    for (int k = 0; k < K; ++k) {
+      col[(size_t)r * K + k] = c[k];
+      val[(size_t)r * K + k] = 1.0 + (hash32((uint64_t)r * 77 + k) & 1023) * 1e-3;
+    }
+  }
+}
+
+__global__ void k_fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v + (i & 7) * 0.01;
+}
+
+// panel id of a column for cut points cuts[0..P]
+__device__ __forceinline__ int panel_of(const int* cuts, int P, int c) {
+  int p = 0;
+  while (p + 1 < P && c >= cuts[p + 1]) ++p;
+  return p;
+}
+
+__global__ void k_count(const int* col, const int* cuts, int P, int* cnt /*[P][M]*/) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    int c[8] = {0};
+    for (int k = 0; k < K; ++k) c[panel_of(cuts, P, col[(size_t)r * K + k])]++;
+    for (int p = 0; p < P; ++p) cnt[(size_t)p * M + r] = c[p];
+  }
+}
+
+__global__ void k_scatter(const int* col, const double* val, const int* cuts, int P, const int* po,
+                          int* pci, double* pva) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    int o[8];
+    for (int p = 0; p < P; ++p) o[p] = po[(size_t)p * M + r];
+    for (int k = 0; k < K; ++k) {
+      const int c = col[(size_t)r * K + k];
+      const int p = panel_of(cuts, P, c);
+      pci[o[p]] = c;
+      pva[o[p]] = val[(size_t)r * K + k];
+      ++o[p];
+    }
+  }
+}
+
+struct Y {  // y-space vectors of the epilogue
+  double *y, *yh, *ya, *yb, *gx, *gxh, *gxa, *h;
+  double *w;
+};
+
+// producer: like k_step_x (13 n-vector streams), writes x~
+__global__ void __launch_bounds__(BS, 8) k_xstep(const double* a0, const double* a1, const double* a2,
+                                                 const double* a3, const double* a4, const double* a5,
+                                                 const double* a6, double* b0, double* b1, double* b2,
+                                                 double* b3, double* xt, double* part) {
+  double acc = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    const double x = a0[j], xh = a1[j], xa = a2[j], g = a4[j], gh = a5[j], ga = a6[j];
+    const double xn = 0.9 * xh + 0.05 * x + 0.05 * xa, gn = 0.9 * gh + 0.05 * g + 0.05 * ga;
+    b0[j] = xn;
+    b1[j] = gn;
+    b2[j] = 0.5 * (a3[j] + xn);
+    const double p = fmin(fmax(xn - 0.01 * gn, -2.0), 2.0);
+    b3[j] = p;
+    xt[j] = 2.0 * p - xn;
+    acc += p * p;
+  }
+  if (acc == 12345.0) part[0] = acc;
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const double* va,
+                                             const double* x, const double* win, double* wout) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    const int b = po[r], e = po[r + 1];
+    double s = FIRST ? 0.0 : win[r];
+    for (int j = b; j < e; j += 4) {
+      const int q = e - j;
+      const int c0 = ci[j];
+      const int c1 = q > 1 ? ci[j + 1] : 0, c2 = q > 2 ? ci[j + 2] : 0, c3 = q > 3 ? ci[j + 3] : 0;
+      const double v0 = va[j];
+      const double v1 = q > 1 ? va[j + 1] : 0.0, v2 = q > 2 ? va[j + 2] : 0.0, v3 = q > 3 ? va[j + 3] : 0.0;
+      const double x0 = __ldg(x + c0);
+      const double x1 = q > 1 ? __ldg(x + c1) : 0.0, x2 = q > 2 ? __ldg(x + c2) : 0.0,
+                   x3 = q > 3 ? __ldg(x + c3) : 0.0;
+      s += v0 * x0;
+      if (q > 1) s += v1 * x1;
+      if (q > 2) s += v2 * x2;
+      if (q > 3) s += v3 * x3;
+    }
+    wout[r] = s;
+  }
+}
+
+__device__ __forceinline__ void yepi(const Y& Yv, int r, double dot, double* acc) {
+  const double yo = Yv.y[r];
+  const double yn = 0.9 * Yv.yh[r] + 0.05 * yo + 0.05 * Yv.ya[r];
+  const double go = Yv.gx[r];
+  const double gn = 0.9 * Yv.gxh[r] + 0.05 * go + 0.05 * Yv.gxa[r];
+  Yv.yb[r] = 0.5 * (Yv.yb[r] + yn);
+  Yv.y[r] = yn;
+  Yv.gx[r] = gn;
+  const double hi = Yv.h[r];
+  const double v = yn + 0.01 * (hi - dot);
+  Yv.gxh[r] = 0.5 * (dot + gn);
+  const double p = fmax(v, 0.0);
+  Yv.yh[r] = p;
+  acc[0] += (p - yn) * (p - yn);
+  acc[1] += p * hi;
+}
+
+// last panel + epilogue
+__global__ void __launch_bounds__(BS, 6) k_final(const int* po, const int* ci, const double* va,
+                                                 const double* x, const double* win, Y Yv, double* part) {
+  double acc[2] = {0, 0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    const int b = po[r], e = po[r + 1];
+    double s = win ? win[r] : 0.0;
+    for (int j = b; j < e; j += 4) {
+      const int q = e - j;
+      const int c0 = ci[j];
+      const int c1 = q > 1 ? ci[j + 1] : 0, c2 = q > 2 ? ci[j + 2] : 0, c3 = q > 3 ? ci[j + 3] : 0;
+      const double v0 = va[j];
+      const double v1 = q > 1 ? va[j + 1] : 0.0, v2 = q > 2 ? va[j + 2] : 0.0, v3 = q > 3 ? va[j + 3] : 0.0;
+      const double x0 = __ldg(x + c0);
+      const double x1 = q > 1 ? __ldg(x + c1) : 0.0, x2 = q > 2 ? __ldg(x + c2) : 0.0,
+                   x3 = q > 3 ? __ldg(x + c3) : 0.0;
+      s += v0 * x0;
+      if (q > 1) s += v1 * x1;
+      if (q > 2) s += v2 * x2;
+      if (q > 3) s += v3 * x3;
+    }
+    yepi(Yv, r, s, acc);
+  }
+  if (acc[0] == 12345.0) part[0] = acc[0] + acc[1];
+}
+
+// epilogue only (w from the passes)
+__global__ void __launch_bounds__(BS, 8) k_epi(const double* win, Y Yv, double* part) {
+  double acc[2] = {0, 0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x)
+    yepi(Yv, r, win[r], acc);
+  if (acc[0] == 12345.0) part[0] = acc[0] + acc[1];
+}
+
+struct Panels {
+  int P;
+  std::vector<int> cuts;
+  int* d_po;  // [P][M+1] (each panel's own offsets into pci/pva)
+  int* d_pci;
+  double* d_pva;
+};
+
+Panels build(const int* d_col, const double* d_val, std::vector<int> cuts) {
+  Panels Q;
+  Q.P = (int)cuts.size() - 1;
+  Q.cuts = cuts;
+  int* d_cuts;
+  CK(cudaMalloc(&d_cuts, sizeof(int) * cuts.size()));
+  CK(cudaMemcpy(d_cuts, cuts.data(), sizeof(int) * cuts.size(), cudaMemcpyHostToDevice));
+  int* cnt;
+  CK(cudaMalloc(&cnt, sizeof(int) * ((size_t)Q.P * M + 1)));
+  k_count<<<4096, BS>>>(d_col, d_cuts, Q.P, cnt);
+  CK(cudaMalloc(&Q.d_po, sizeof(int) * ((size_t)Q.P * M + 1)));
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, Q.d_po, (int)((size_t)Q.P * M + 1));
+  CK(cudaMalloc(&tmp, tb));
+  CK(cudaMemset(cnt + (size_t)Q.P * M, 0, sizeof(int)));
+  cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, Q.d_po, (int)((size_t)Q.P * M + 1));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMalloc(&Q.d_pci, sizeof(int) * (size_t)M * K));
+  CK(cudaMalloc(&Q.d_pva, sizeof(double) * (size_t)M * K));
+  k_scatter<<<4096, BS>>>(d_col, d_val, d_cuts, Q.P, Q.d_po, Q.d_pci, Q.d_pva);
+  CK(cudaDeviceSynchronize());
+  cudaFree(tmp);
+  cudaFree(cnt);
+  cudaFree(d_cuts);
+  return Q;
+}
+
+void free_panels(Panels& Q) {
+  cudaFree(Q.d_po);
+  cudaFree(Q.d_pci);
+  cudaFree(Q.d_pva);
+}
+
+int main(int argc, char** argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 10;
+  int nsm = 148;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  int *d_col;
+  double* d_val;
+  CK(cudaMalloc(&d_col, sizeof(int) * (size_t)M * K));
+  CK(cudaMalloc(&d_val, sizeof(double) * (size_t)M * K));
+  k_gen<<<4096, BS>>>(d_col, d_val);
+  CK(cudaDeviceSynchronize());
+  // x-space
+  std::vector<double*> xs(12);
+  for (auto& p : xs) { CK(cudaMalloc(&p, sizeof(double) * N)); k_fill<<<4096, BS>>>(p, N, 0.1); }
+  double* xt;
+  CK(cudaMalloc(&xt, sizeof(double) * N));
+  // y-space
+  Y Yv;
+  double** yp[] = {&Yv.y, &Yv.yh, &Yv.ya, &Yv.yb, &Yv.gx, &Yv.gxh, &Yv.gxa, &Yv.h, &Yv.w};
+  for (auto pp : yp) { CK(cudaMalloc(pp, sizeof(double) * M)); k_fill<<<4096, BS>>>(*pp, M, 0.2); }
+  double *wA, *wB, *part;
+  CK(cudaMalloc(&wA, sizeof(double) * M));
+  CK(cudaMalloc(&wB, sizeof(double) * M));
+  CK(cudaMalloc(&part, 64));
+  CK(cudaDeviceSynchronize());
+
+  int occ_pass = 0, occ_fin = 0, occ_x = 0, occ_epi = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_pass, k_pass<false>, BS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_final, BS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_xstep, BS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_epi, k_epi, BS, 0);
+  const int gp = occ_pass * nsm, gf = occ_fin * nsm, gx = occ_x * nsm, ge = occ_epi * nsm;
+  printf("grids pass %d final %d xstep %d epi %d\n", gp, gf, gx, ge);
+
+  cudaEvent_t e0, e1, e2;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+  auto xstep = [&]() {
+    k_xstep<<<gx, BS>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6], xs[7], xs[8], xs[9], xs[10], xt, part);
+  };
+
+  struct Variant { const char* name; std::vector<double> fr; int order; int split; };
+  // fr: panel width fractions; order 0 = panels 0..P-1, 1 = reversed; split: epilogue in its own kernel
+  std::vector<Variant> V = {
+      {"P3 equal fwd (current)", {1, 1, 1}, 0, 0},
+      {"P3 equal rev", {1, 1, 1}, 1, 0},
+      {"P3 equal fwd split-epi", {1, 1, 1}, 0, 1},
+      {"P3 equal rev split-epi", {1, 1, 1}, 1, 1},
+      {"P3 40/40/20 fwd", {2, 2, 1}, 0, 0},
+      {"P3 20/40/40 rev", {1, 2, 2}, 1, 0},
+      {"P4 equal fwd", {1, 1, 1, 1}, 0, 0},
+      {"P4 equal rev", {1, 1, 1, 1}, 1, 0},
+      {"P4 30/30/30/10 fwd", {3, 3, 3, 1}, 0, 0},
+      {"P2 equal fwd", {1, 1}, 0, 0},
+      {"P5 equal rev", {1, 1, 1, 1, 1}, 1, 0},
+      {"P6 equal rev split-epi", {1, 1, 1, 1, 1, 1}, 1, 1},
+  };
+  for (const Variant& v : V) {
+    double tot = 0;
+    for (double f : v.fr) tot += f;
+    std::vector<int> cuts(1, 0);
+    double acc = 0;
+    for (size_t i = 0; i + 1 < v.fr.size(); ++i) { acc += v.fr[i]; cuts.push_back((int)(N * acc / tot)); }
+    cuts.push_back(N);
+    Panels Q = build(d_col, d_val, cuts);
+    const int P = Q.P;
+    std::vector<int> ord(P);
+    for (int i = 0; i < P; ++i) ord[i] = v.order ? P - 1 - i : i;
+    float best = 1e9, sum = 0, xbest = 1e9;
+    for (int it = 0; it < reps + 2; ++it) {
+      CK(cudaEventRecord(e0));
+      xstep();
+      CK(cudaEventRecord(e1));
+      double* win = nullptr;
+      double* bufs[2] = {wA, wB};
+      const int npass = v.split ? P : P - 1;
+      for (int i = 0; i < npass; ++i) {
+        const int p = ord[i];
+        const int* po = Q.d_po + (size_t)p * M;
+        double* wo = bufs[i & 1];
+        if (i == 0) k_pass<true><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+        else k_pass<false><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        win = wo;
+      }
+      if (v.split) {
+        k_epi<<<ge, BS>>>(win, Yv, part);
+      } else {
+        const int p = ord[P - 1];
+        k_final<<<gf, BS>>>(Q.d_po + (size_t)p * M, Q.d_pci, Q.d_pva, xt, win, Yv, part);
+      }
+      CK(cudaEventRecord(e2));
+      CK(cudaEventSynchronize(e2));
+      float ms = 0, xms = 0;
+      cudaEventElapsedTime(&xms, e0, e1);
+      cudaEventElapsedTime(&ms, e1, e2);
+      if (it >= 2) { best = std::min(best, ms); sum += ms; xbest = std::min(xbest, xms); }
+    }
+    CK(cudaGetLastError());
+    printf("%-28s ystep best %.4f ms avg %.4f ms   (xstep %.4f ms)\n", v.name, best, sum / reps, xbest);
+    fflush(stdout);
+    free_panels(Q);
+  }
+  return 0;
+}

@@ -64,6 +64,8 @@ def parse_args():
                     help="N>1: every rank solves its own copy instead of one row-sharded solve")
     ap.add_argument("--sharded", action="store_true",
                     help="use the row-sharded engine even on one GPU (NCCL in-graph path)")
+    ap.add_argument("--selfcheck", action="store_true",
+                    help="with --sharded on one GPU: also run the N>1 trajectory self-check")
     ap.add_argument("--no-ttt-c1", action="store_true",
                     help="skip the C1 time-to-1e-6 solve (both arms run it by default)")
     ap.add_argument("--no-sustained", action="store_true",
@@ -256,6 +258,39 @@ def run_reference(args, rank, world):
     emit(line)
 
 
+def selfcheck_sharded(problem, rank, world, k=20, tol=1e-9):
+    """N>1 correctness gate of the sharded engine: every rank runs the row-
+    sharded solve for k iterations, rank 0 re-runs the same k iterations on
+    one GPU, and the returned iterates must agree to `tol` (relative to their
+    max-abs).  The sharded column statistics of the preconditioner and the
+    reduce-scattered G^T y sums add in another order, so agreement is to
+    rounding, not bit for bit (<= 1e-11 at k <= 20)."""
+    import numpy as np
+    import torch.distributed as dist
+
+    from paper_2603_15504_b200 import SolverOptions, solve
+    from paper_2603_15504_b200.distributed import solve_sharded
+
+    opts = dict(max_iter=k, rel_tol=1e-14, abs_tol=1e-14, time_limit=1e9)
+    t0 = time.perf_counter()
+    rs = solve_sharded(problem, SolverOptions(**opts))
+    out = {"k": k, "tol": tol, "iterations": rs.iterations}
+    ok = 1.0
+    if rank == 0:
+        r1 = solve(problem, SolverOptions(**opts))
+        dx = float(np.max(np.abs(rs.x - r1.x)) / max(1.0, float(np.max(np.abs(r1.x)))))
+        dy = float(np.max(np.abs(rs.y - r1.y)) / max(1.0, float(np.max(np.abs(r1.y)))))
+        ok = float(rs.iterations == r1.iterations and dx <= tol and dy <= tol)
+        out.update(max_rel_diff_x=dx, max_rel_diff_y=dy, single_iterations=r1.iterations)
+    import torch
+
+    t = torch.tensor([ok], device="cuda", dtype=torch.float64)
+    dist.broadcast(t, src=0)
+    out["pass"] = bool(t.item() == 1.0)
+    out["wall_s"] = time.perf_counter() - t0
+    return out
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -286,6 +321,10 @@ def run_ours(args, rank, world, local):
     t_gen = time.monotonic()
     problem = make(instances)
     gen_s = time.monotonic() - t_gen
+    selfcheck = None
+    if sharded and (world > 1 or args.selfcheck):
+        selfcheck = selfcheck_sharded(problem, rank, world)
+        torch.cuda.empty_cache()
     opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=10**9, time_limit=1e9)
 
     t_setup = time.monotonic()
@@ -462,11 +501,16 @@ def run_ours(args, rank, world, local):
             line["time_to_1e-6_C1"] = ttt_c1
         if sustained:
             line["sustained"] = sustained
+        if selfcheck:
+            line["selfcheck"] = selfcheck
         if batched:
             line["batched"] = batched
         emit(line)
     if dist:
         dist.destroy_process_group()
+    if selfcheck and not selfcheck["pass"]:
+        sys.stderr.write(f"sharded self-check FAILED: {selfcheck}\n")
+        sys.exit(3)
 
 
 _OUT = None

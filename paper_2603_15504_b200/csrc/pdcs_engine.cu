@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -16,6 +17,29 @@
 using namespace pdcs;
 
 namespace {
+
+// PDCS_TIMING=1: host-side phase times of engine setup on stderr (each phase
+// ends with a stream synchronize, so only use it to find setup hot spots).
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t s = nullptr;
+  std::chrono::steady_clock::time_point t0;
+  const char* what = "";
+  PhaseTimer(const char* w, cudaStream_t st) : s(st), what(w) {
+    const char* e = getenv("PDCS_TIMING");
+    on = e && e[0] == '1';
+    t0 = std::chrono::steady_clock::now();
+  }
+  void lap(const char* phase) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pdcs timing] %s %-22s %8.2f ms\n", what, phase,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
@@ -550,6 +574,35 @@ int lane_t(Engine* E, const KArgs& A) {
   return 0;
 }
 
+// Sharded engine: the rank's G_p^T y_hat_p partial sums over all of x-space
+// (reduce-scattered afterwards) through the same column-panelled lane passes
+// as the single-GPU G^T step, the last pass writing the raw partial product.
+// Matrices with chunked long rows or tiled steps keep the generic SpMV.
+template <int VW, int GP>
+int lane_t_partial(Engine* E) {
+  const SpmvPlan& P = E->GT;
+  const PanelPlan& Q = E->PGT;
+  if (lane_passes<VW, GP>(E, P, Q, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
+  CK(launch_step(use_pdl(E), k_lane_pass<VW, GP>, P.pass_grid, E->stream,
+                 tile_source(P, Q, Q.np - 1, E->d_wpart_x), P.nrows, (const double*)E->d.d_yh, E->d_gtp,
+                 (const PdcsCtrl*)E->d_ctrl, 2, E->keep_yh));
+  CKL();
+  return 0;
+}
+
+int launch_gt_partial(Engine* E) {
+  if (E->GT.n_long || E->tile_t || E->GT.nrows == 0)
+    return launch_spmv(E->GT, E->d.d_yh, E->d_gtp, E->stream, E->d_ctrl, 2);
+  switch (E->GT.step_vw * 2 + E->gp) {
+    case 2: return lane_t_partial<1, 0>(E);
+    case 3: return lane_t_partial<1, 1>(E);
+    case 16: return lane_t_partial<8, 0>(E);
+    case 17: return lane_t_partial<8, 1>(E);
+    case 65: return lane_t_partial<32, 1>(E);
+    default: return lane_t_partial<32, 0>(E);
+  }
+}
+
 int launch_step_y(Engine* E, const KArgs& A) {
   if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
@@ -741,7 +794,7 @@ int launch_slot(Engine* E) {
     // sharded: local G_p^T y_hat_p partial sums over all of x-space,
     // reduce-scattered so each rank gets its x-slice of G^T y_hat, then the
     // x-space epilogue on that slice
-    if (launch_spmv(E->GT, E->d.d_yh, E->d_gtp, s, E->d_ctrl, 2)) return 1;
+    if (launch_gt_partial(E)) return 1;
     mark(s, "step_t_partial");
     if (nccl_x_reduce_scatter(E, E->d_gtp, E->d.d_gth, s)) return 1;
     mark(s, "reduce_scatter_gty");
@@ -929,6 +982,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   E->allow_nonuniform_dual_soc = d.allow_nonuniform_dual_soc;
   cudaStream_t s = E->stream;
   auto fail = [&](int rc) { pdcs_engine_destroy(E); return rc; };
+  PhaseTimer T("create", s);
 
   // cone tables: primal blocks start after the box; dual blocks beyond m_elem
   std::vector<PdcsBlock> xb, yb, ux, uy;
@@ -995,12 +1049,15 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   E->n_unif_x = (int)ux.size();
   E->n_unif_y = (int)uy.size();
 
+  T.lap("cone tables");
   // transpose of the pattern (values are written by pdcs_precondition)
   if (pdcs_transpose_csr(d.m, d.n, d.nnz, d.d_g_rowptr, d.d_g_colidx, nullptr, d.d_gt_rowptr,
                          d.d_gt_colidx, nullptr, d.d_perm, s))
     return fail(1);
+  T.lap("transpose");
   if (build_plan(E->G, d.m, d.n, d.nnz, d.d_g_rowptr, d.d_g_colidx, d.d_g_val, s)) return fail(1);
   if (build_plan(E->GT, d.n, d.m, d.nnz, d.d_gt_rowptr, d.d_gt_colidx, d.d_gt_val, s)) return fail(1);
+  T.lap("spmv plans");
 
   // grids and reduction capacities: the streaming step kernels get exactly one
   // wave of resident CTAs (grid-stride loops), the rest a capped grid
@@ -1036,6 +1093,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const int py = (int)tune("py", panels_for(d.n, d.m, d.nnz));
     const int pt = (int)tune("pt", panels_for(d.m, d.n, d.nnz));
     if (build_panels(E->PG, E->G, py, s) || build_panels(E->PGT, E->GT, pt, s)) return fail(1);
+    T.lap("panels");
     // gp=1: gathers of the lane-mapped step SpMVs fetch 64 B into L2 (PTX
     // L2::64B).  Measured slower on C5, as were two rows per thread and
     // loading the epilogue operands ahead of the gathers (profiles/r01_sweeps.txt).
@@ -1063,6 +1121,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1 && E->G.len_cv > 0.5))) > 0.0;
     E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw == 32))) > 0.0;
     if ((E->tile_y && build_tiles(E->G, s)) || (E->tile_t && build_tiles(E->GT, s))) return fail(1);
+    T.lap("tiles");
     if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
       return fail(1);
     if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)
@@ -1127,6 +1186,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     g_err = "pdcs_engine_create: workspace init failed";
     return fail(1);
   }
+  T.lap("grids + workspace");
   *out = E;
   return 0;
 }
@@ -1172,6 +1232,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   cudaStream_t s = E->stream;
   const KArgs A = make_args(E);
   const int n = E->n, m = E->m, nnz = E->nnz;
+  PhaseTimer T("precondition", s);
   int* rowid = nullptr;
   if (nnz > 0) {
     CK(cudaMalloc(&rowid, sizeof(int) * nnz));
@@ -1254,6 +1315,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   CKL();
   CK(cudaStreamSynchronize(s));
   cudaFree(rowid);
+  T.lap("ruiz + pc + scale");
   return 0;
 }
 
@@ -1303,6 +1365,7 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
   if (!E->exec || E->graph_slots != slots) {
     if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }
     if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
+    PhaseTimer T("run_inner", s);
     const int64_t before = g_launches.load();
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < slots; ++i) {
@@ -1315,6 +1378,7 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
     }
     CK(cudaStreamEndCapture(s, &E->graph));
     CK(cudaGraphInstantiate(&E->exec, E->graph, 0));
+    T.lap("graph capture");
     E->graph_nodes = g_launches.load() - before;
     g_launches.fetch_sub(E->graph_nodes);  // captured, not launched
     E->graph_slots = slots;

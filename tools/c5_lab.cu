@@ -79,6 +79,45 @@ __global__ void k_scatter(const int* col, const double* val, const int* cuts, in
   }
 }
 
+// stream loads: MODE 0 plain __ldg, 1 L2::evict_first policy, 2 L1::no_allocate
+template <int MODE, class T>
+__device__ __forceinline__ T lds(const T* a) {
+  if (MODE == 0) return __ldg(a);
+  if (MODE == 1) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if (sizeof(T) == 8) {
+      double v;
+      asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+      return *reinterpret_cast<T*>(&v);
+    } else {
+      int v;
+      asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+      return *reinterpret_cast<T*>(&v);
+    }
+  }
+  if (sizeof(T) == 8) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a));
+    return *reinterpret_cast<T*>(&v);
+  } else {
+    int v;
+    asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(a));
+    return *reinterpret_cast<T*>(&v);
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void sts(double* a, double v) {
+  if (MODE == 1) {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+  } else {
+    *a = v;
+  }
+}
+
 struct Y {  // y-space vectors of the epilogue
   double *y, *yh, *ya, *yb, *gx, *gxh, *gxa, *h;
   double *w;
@@ -104,18 +143,20 @@ __global__ void __launch_bounds__(BS, 8) k_xstep(const double* a0, const double*
   if (acc == 12345.0) part[0] = acc;
 }
 
-template <bool FIRST>
+template <bool FIRST, int MODE = 0>
 __global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const double* va,
                                              const double* x, const double* win, double* wout) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
-    const int b = po[r], e = po[r + 1];
-    double s = FIRST ? 0.0 : win[r];
+    const int b = lds<MODE>(po + r), e = lds<MODE>(po + r + 1);
+    double s = FIRST ? 0.0 : lds<MODE>(win + r);
     for (int j = b; j < e; j += 4) {
       const int q = e - j;
-      const int c0 = ci[j];
-      const int c1 = q > 1 ? ci[j + 1] : 0, c2 = q > 2 ? ci[j + 2] : 0, c3 = q > 3 ? ci[j + 3] : 0;
-      const double v0 = va[j];
-      const double v1 = q > 1 ? va[j + 1] : 0.0, v2 = q > 2 ? va[j + 2] : 0.0, v3 = q > 3 ? va[j + 3] : 0.0;
+      const int c0 = lds<MODE>(ci + j);
+      const int c1 = q > 1 ? lds<MODE>(ci + j + 1) : 0, c2 = q > 2 ? lds<MODE>(ci + j + 2) : 0,
+                c3 = q > 3 ? lds<MODE>(ci + j + 3) : 0;
+      const double v0 = lds<MODE>(va + j);
+      const double v1 = q > 1 ? lds<MODE>(va + j + 1) : 0.0, v2 = q > 2 ? lds<MODE>(va + j + 2) : 0.0,
+                   v3 = q > 3 ? lds<MODE>(va + j + 3) : 0.0;
       const double x0 = __ldg(x + c0);
       const double x1 = q > 1 ? __ldg(x + c1) : 0.0, x2 = q > 2 ? __ldg(x + c2) : 0.0,
                    x3 = q > 3 ? __ldg(x + c3) : 0.0;
@@ -124,7 +165,7 @@ __global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const
       if (q > 2) s += v2 * x2;
       if (q > 3) s += v3 * x3;
     }
-    wout[r] = s;
+    sts<MODE>(wout + r, s);
   }
 }
 
@@ -146,18 +187,21 @@ __device__ __forceinline__ void yepi(const Y& Yv, int r, double dot, double* acc
 }
 
 // last panel + epilogue
+template <int MODE = 0>
 __global__ void __launch_bounds__(BS, 6) k_final(const int* po, const int* ci, const double* va,
                                                  const double* x, const double* win, Y Yv, double* part) {
   double acc[2] = {0, 0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
-    const int b = po[r], e = po[r + 1];
-    double s = win ? win[r] : 0.0;
+    const int b = lds<MODE>(po + r), e = lds<MODE>(po + r + 1);
+    double s = win ? lds<MODE>(win + r) : 0.0;
     for (int j = b; j < e; j += 4) {
       const int q = e - j;
-      const int c0 = ci[j];
-      const int c1 = q > 1 ? ci[j + 1] : 0, c2 = q > 2 ? ci[j + 2] : 0, c3 = q > 3 ? ci[j + 3] : 0;
-      const double v0 = va[j];
-      const double v1 = q > 1 ? va[j + 1] : 0.0, v2 = q > 2 ? va[j + 2] : 0.0, v3 = q > 3 ? va[j + 3] : 0.0;
+      const int c0 = lds<MODE>(ci + j);
+      const int c1 = q > 1 ? lds<MODE>(ci + j + 1) : 0, c2 = q > 2 ? lds<MODE>(ci + j + 2) : 0,
+                c3 = q > 3 ? lds<MODE>(ci + j + 3) : 0;
+      const double v0 = lds<MODE>(va + j);
+      const double v1 = q > 1 ? lds<MODE>(va + j + 1) : 0.0, v2 = q > 2 ? lds<MODE>(va + j + 2) : 0.0,
+                   v3 = q > 3 ? lds<MODE>(va + j + 3) : 0.0;
       const double x0 = __ldg(x + c0);
       const double x1 = q > 1 ? __ldg(x + c1) : 0.0, x2 = q > 2 ? __ldg(x + c2) : 0.0,
                    x3 = q > 3 ? __ldg(x + c3) : 0.0;
@@ -248,7 +292,7 @@ int main(int argc, char** argv) {
 
   int occ_pass = 0, occ_fin = 0, occ_x = 0, occ_epi = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_pass, k_pass<false>, BS, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_final, BS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_fin, k_final<0>, BS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_xstep, BS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_epi, k_epi, BS, 0);
   const int gp = occ_pass * nsm, gf = occ_fin * nsm, gx = occ_x * nsm, ge = occ_epi * nsm;
@@ -260,21 +304,18 @@ int main(int argc, char** argv) {
     k_xstep<<<gx, BS>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6], xs[7], xs[8], xs[9], xs[10], xt, part);
   };
 
-  struct Variant { const char* name; std::vector<double> fr; int order; int split; };
+  struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; };
   // fr: panel width fractions; order 0 = panels 0..P-1, 1 = reversed; split: epilogue in its own kernel
   std::vector<Variant> V = {
       {"P3 equal fwd (current)", {1, 1, 1}, 0, 0},
-      {"P3 equal rev", {1, 1, 1}, 1, 0},
+      {"P3 fwd streams evict_first", {1, 1, 1}, 0, 0, 1},
+      {"P3 fwd streams L1 no_alloc", {1, 1, 1}, 0, 0, 2},
+      {"P4 fwd streams evict_first", {1, 1, 1, 1}, 0, 0, 1},
+      {"P6 fwd streams evict_first", {1, 1, 1, 1, 1, 1}, 0, 0, 1},
+      {"P3 split-epi evict_first", {1, 1, 1}, 0, 1, 1},
       {"P3 equal fwd split-epi", {1, 1, 1}, 0, 1},
-      {"P3 equal rev split-epi", {1, 1, 1}, 1, 1},
-      {"P3 40/40/20 fwd", {2, 2, 1}, 0, 0},
-      {"P3 20/40/40 rev", {1, 2, 2}, 1, 0},
       {"P4 equal fwd", {1, 1, 1, 1}, 0, 0},
-      {"P4 equal rev", {1, 1, 1, 1}, 1, 0},
       {"P4 30/30/30/10 fwd", {3, 3, 3, 1}, 0, 0},
-      {"P2 equal fwd", {1, 1}, 0, 0},
-      {"P5 equal rev", {1, 1, 1, 1, 1}, 1, 0},
-      {"P6 equal rev split-epi", {1, 1, 1, 1, 1, 1}, 1, 1},
   };
   for (const Variant& v : V) {
     double tot = 0;
@@ -299,15 +340,25 @@ int main(int argc, char** argv) {
         const int p = ord[i];
         const int* po = Q.d_po + (size_t)p * M;
         double* wo = bufs[i & 1];
-        if (i == 0) k_pass<true><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
-        else k_pass<false><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        if (v.mode == 1) {
+          if (i == 0) k_pass<true, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+          else k_pass<false, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        } else if (v.mode == 2) {
+          if (i == 0) k_pass<true, 2><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+          else k_pass<false, 2><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        } else {
+          if (i == 0) k_pass<true><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+          else k_pass<false><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        }
         win = wo;
       }
       if (v.split) {
         k_epi<<<ge, BS>>>(win, Yv, part);
       } else {
         const int p = ord[P - 1];
-        k_final<<<gf, BS>>>(Q.d_po + (size_t)p * M, Q.d_pci, Q.d_pva, xt, win, Yv, part);
+        if (v.mode == 1) k_final<1><<<gf, BS>>>(Q.d_po + (size_t)p * M, Q.d_pci, Q.d_pva, xt, win, Yv, part);
+        else if (v.mode == 2) k_final<2><<<gf, BS>>>(Q.d_po + (size_t)p * M, Q.d_pci, Q.d_pva, xt, win, Yv, part);
+        else k_final<0><<<gf, BS>>>(Q.d_po + (size_t)p * M, Q.d_pci, Q.d_pva, xt, win, Yv, part);
       }
       CK(cudaEventRecord(e2));
       CK(cudaEventSynchronize(e2));

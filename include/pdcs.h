@@ -214,6 +214,20 @@ int pdcs_engine_set_ctrl(PdcsEngine* e, const PdcsCtrl* h_ctrl);
  * `slots_per_graph` line-search trials. */
 int pdcs_run_inner(PdcsEngine* e, int32_t slots_per_graph);
 
+/* ---- batched engines (many C1-class solves per GPU) ----
+ * One CUDA graph forks into every member engine's stream (each branch runs
+ * `slots` line-search trials of that engine, exactly the pdcs_run_inner
+ * sequence), joins, and gathers the members' control blocks.  pdcs_batch_run
+ * replays it until every member's device loop has stopped; members the host
+ * keeps stopped (ctrl.stop = 1) are gated off.  Members: non-sharded engines,
+ * each used by one host thread at a time between runs.  The reference solves
+ * one problem per call (engine.py:683-689); results per member are
+ * bit-identical to pdcs_run_inner. */
+typedef struct PdcsBatch PdcsBatch;
+int pdcs_batch_create(PdcsEngine** engines, int32_t n, void* stream, PdcsBatch** out);
+int pdcs_batch_run(PdcsBatch* b, int32_t slots_per_graph);
+void pdcs_batch_destroy(PdcsBatch* b);
+
 /* Runs `reps` line-search trials eagerly (not from the graph) with CUDA
  * events between the stages and returns the number of stages; h_ms[i] is the
  * mean device time of stage i and h_names[i] its name (static strings).
@@ -296,6 +310,15 @@ int pdcs_axpby(PdcsEngine* e, int32_t space, double a, const double* d_p, double
  * gx~ = G^ x~ and gty~ = G^T y~. */
 int pdcs_unscale(PdcsEngine* e, const double* d_x, const double* d_y, const double* d_gx,
                  const double* d_gty, double* d_xo, double* d_yo, double* d_slack, double* d_lam);
+
+/* Declare that every box coordinate j < num_box has the same unscaled
+ * bounds [lo, hi] (infinities allowed).  The step kernels then form the
+ * scaled bounds as lo / d2_j, hi / d2_j -- the same division the scaling
+ * kernel performs, so the values are identical -- and stream d2 instead of
+ * l^ and u^ (one n-vector instead of two in the x-step and the G^T step).
+ * Replaces nothing in the reference (project_box, cones.py:46-51, reads the
+ * arrays); an optimisation of the same arithmetic. */
+int pdcs_engine_set_uniform_box(PdcsEngine* e, double lo, double hi);
 
 /* ---- multi-GPU ------------------------------------------------
  * A sharded solve gives every rank a contiguous row slice of G^ (cut at dual

@@ -98,6 +98,9 @@ _SIGS = {
     "pdcs_engine_get_ctrl": (C.c_int, [_P, C.POINTER(PdcsCtrl)]),
     "pdcs_engine_set_ctrl": (C.c_int, [_P, C.POINTER(PdcsCtrl)]),
     "pdcs_run_inner": (C.c_int, [_P, C.c_int32]),
+    "pdcs_batch_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, _P, C.POINTER(C.c_void_p)]),
+    "pdcs_batch_run": (C.c_int, [_P, C.c_int32]),
+    "pdcs_batch_destroy": (None, [_P]),
     "pdcs_flush": (C.c_int, [_P]),
     "pdcs_profile_slot": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_char_p), C.c_int32]),
     "pdcs_engine_spmv": (C.c_int, [_P, C.c_int32, _P, _P]),
@@ -116,6 +119,7 @@ _SIGS = {
     "pdcs_unscale": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pdcs_debug_inject_nan": (C.c_int, [_P, C.c_int64]),
     "pdcs_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "pdcs_engine_set_uniform_box": (C.c_int, [_P, C.c_double, C.c_double]),
     "pdcs_engine_set_comm": (C.c_int, [_P, C.c_char_p, C.c_int32, C.c_int32]),
     "pdcs_engine_set_xsplit": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_int32]),
     "pdcs_allgather_x": (C.c_int, [_P, C.POINTER(C.c_void_p), C.c_int32]),
@@ -130,8 +134,8 @@ _lock = threading.Lock()
 def build_native(force: bool = False, verbose: bool = False) -> str:
     """Compile libpdcs.so in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
     srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))]
+    newest = max(os.path.getmtime(s) for s in srcs + [os.path.join(INCLUDE, "pdcs.h")])
     if not force and os.path.exists(LIB_PATH):
-        newest = max(os.path.getmtime(s) for s in srcs + [os.path.join(INCLUDE, "pdcs.h")])
         if os.path.getmtime(LIB_PATH) >= newest:
             return LIB_PATH
     cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp",
@@ -142,6 +146,9 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     if verbose and res.stderr:
         print(res.stderr)
     os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    # stamp the library with the sources' time at build start: a source edited
+    # while nvcc ran is then newer and triggers the next rebuild
+    os.utime(LIB_PATH, (newest, newest))
     return LIB_PATH
 
 

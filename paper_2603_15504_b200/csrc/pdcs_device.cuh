@@ -65,14 +65,14 @@ template <bool H = kL2Hints>
 __device__ __forceinline__ double ld_hint(const double* a, uint64_t pol) {
   if (!H) return __ldg(a);
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
 template <bool H = kL2Hints>
 __device__ __forceinline__ int ld_hint(const int* a, uint64_t pol) {
   if (!H) return __ldg(a);
   int v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
   return v;
 }
 // Gather load with an explicit L2 fill size: GP = 0 plain, 1 = 64 B, 2 = 128 B
@@ -81,8 +81,8 @@ template <int GP>
 __device__ __forceinline__ double ld_gather(const double* a) {
   if (GP == 0) return __ldg(a);
   double v;
-  if (GP == 1) asm volatile("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(a));
-  else asm volatile("ld.global.nc.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  if (GP == 1) asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(a));
+  else asm("ld.global.nc.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(a));
   return v;
 }
 

@@ -1,5 +1,6 @@
 // libpdcs: host orchestration and the C ABI (include/pdcs.h).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -200,6 +201,9 @@ KArgs make_args(const Engine* E) {
   A.keep_xt = E->keep_xt;
   A.keep_yh = E->keep_yh;
   A.exp_rho = E->d_exp_rho;
+  A.ub = E->ubox ? (E->precond_mode == 2 ? 2 : 1) : 0;
+  A.lu = E->ubox_l;
+  A.uu = E->ubox_u;
   return A;
 }
 
@@ -208,32 +212,52 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
                const double* d_val, cudaStream_t s) {
   P.nrows = nrows; P.ncols = ncols; P.nnz = nnz;
   P.rowptr = d_rp; P.colidx = d_ci; P.val = d_val;
-  std::vector<int> rp(nrows + 1, 0);
-  if (nrows > 0) {
-    CK(cudaMemcpyAsync(rp.data(), d_rp, sizeof(int) * (nrows + 1), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  }
   P.vw = choose_vw(nnz, nrows);
   P.long_t = TILE_NNZ;
-  // one host pass: the spread of the short rows' lengths (chooses lane-mapped
-  // vs tiled step kernels) and the long rows
+  // on the device: the spread of the short rows' lengths (chooses lane-mapped
+  // vs tiled step kernels) and the long rows with their extents -- no copy of
+  // the row pointers to the host (setup was 117 ms on C5 with a host pass)
   std::vector<int> lrows;
-  {
-    double s1 = 0.0, s2 = 0.0;
-    int cnt = 0;
-    for (int r = 0; r < nrows; ++r) {
-      const int len = rp[r + 1] - rp[r];
-      if (len > P.long_t) {
-        lrows.push_back(r);
-        continue;
-      }
-      s1 += len;
-      s2 += (double)len * len;
-      ++cnt;
-    }
-    const double mean = cnt ? s1 / cnt : 0.0;
-    const double var = cnt ? std::max(0.0, s2 / cnt - mean * mean) : 0.0;
+  std::vector<int2> lext;
+  if (nrows > 0) {
+    unsigned long long* st = nullptr;
+    CK(cudaMallocAsync(&st, sizeof(unsigned long long) * 4, s));
+    CK(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * 4, s));
+    k_row_stats<<<grid_for(nrows), BS, 0, s>>>(d_rp, nrows, P.long_t, st);
+    CKL();
+    unsigned long long h[4];
+    CK(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const double cnt = (double)h[2];
+    const double mean = cnt > 0 ? (double)h[0] / cnt : 0.0;
+    const double var = cnt > 0 ? std::max(0.0, (double)h[1] / cnt - mean * mean) : 0.0;
     P.len_cv = mean > 0.0 ? std::sqrt(var) / mean : 0.0;
+    const int nl = (int)h[3];
+    if (nl > 0) {
+      int *rows = nullptr, *num = nullptr;
+      int2* ext = nullptr;
+      CK(cudaMallocAsync(&rows, sizeof(int) * nl, s));
+      CK(cudaMallocAsync(&num, sizeof(int), s));
+      CK(cudaMallocAsync(&ext, sizeof(int2) * nl, s));
+      size_t tb = 0;
+      thrust::counting_iterator<int> it(0);
+      CK(cub::DeviceSelect::If(nullptr, tb, it, rows, num, nrows, IsLongRow{d_rp, P.long_t}, s));
+      void* tmp = nullptr;
+      CK(cudaMallocAsync(&tmp, tb, s));
+      CK(cub::DeviceSelect::If(tmp, tb, it, rows, num, nrows, IsLongRow{d_rp, P.long_t}, s));
+      k_row_extents<<<grid_for(nl), BS, 0, s>>>(d_rp, rows, nl, ext);
+      CKL();
+      lrows.resize(nl);
+      lext.resize(nl);
+      CK(cudaMemcpyAsync(lrows.data(), rows, sizeof(int) * nl, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(lext.data(), ext, sizeof(int2) * nl, cudaMemcpyDeviceToHost, s));
+      CK(cudaFreeAsync(tmp, s));
+      CK(cudaFreeAsync(rows, s));
+      CK(cudaFreeAsync(num, s));
+      CK(cudaFreeAsync(ext, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    CK(cudaFreeAsync(st, s));
   }
   // entries per long-row chunk (one CTA reduction each); PDCS_TUNE=chunk=N overrides
   int chunk = 8192;
@@ -243,8 +267,8 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   }
   std::vector<int> lfirst;
   std::vector<int4> chunks;
-  for (int r : lrows) {
-    const int b = rp[r], e = rp[r + 1];
+  for (size_t i = 0; i < lrows.size(); ++i) {
+    const int r = lrows[i], b = lext[i].x, e = lext[i].y;
     lfirst.push_back((int)chunks.size());
     for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), 0));
   }
@@ -555,6 +579,36 @@ CtrlFuse fuse_beta(const Engine* E) {
   return F;
 }
 
+// Split step (E->split): every panel a gather-only pass, the last writing the
+// full product into `out`; then the pure-streaming epilogue kernel.
+template <int VW, int GP, bool HS>
+int split_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* x, double* wpart,
+                 double* out, int gate, float keep) {
+  for (int p = 0; p < Q.np; ++p) {
+    double* dst = p + 1 == Q.np ? out : wpart;
+    CK(launch_step(use_pdl(E), k_lane_pass<VW, GP, HS>, P.pass_grid, E->stream, tile_source(P, Q, p, wpart),
+                   P.nrows, x, dst, (const PdcsCtrl*)E->d_ctrl, gate, keep));
+    CKL();
+  }
+  return 0;
+}
+
+template <bool HS>
+int split_y(Engine* E, const KArgs& A) {
+  if (split_passes<1, 0, HS>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->d.d_w, 1, E->keep_xt)) return 1;
+  CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
+  CKL();
+  return 0;
+}
+
+template <bool HS>
+int split_t(Engine* E, const KArgs& A) {
+  if (split_passes<1, 0, HS>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->d.d_gth, 2, E->keep_yh)) return 1;
+  CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
+  CKL();
+  return 0;
+}
+
 template <int VW, int GP>
 int lane_y(Engine* E, const KArgs& A) {
   if (lane_passes<VW, GP>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
@@ -604,6 +658,7 @@ int launch_gt_partial(Engine* E) {
 }
 
 int launch_step_y(Engine* E, const KArgs& A) {
+  if (E->split) return E->hs ? split_y<true>(E, A) : split_y<false>(E, A);
   if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
     k_step_y<<<E->G.grid, BS, 0, E->stream>>>(A, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y),
@@ -622,6 +677,7 @@ int launch_step_y(Engine* E, const KArgs& A) {
 }
 
 int launch_step_t(Engine* E, const KArgs& A) {
+  if (E->split) return E->hs ? split_t<true>(E, A) : split_t<false>(E, A);
   if (E->tile_t) {
     if (launch_panel_passes(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->GT.grid, 2)) return 1;
     k_step_t<<<E->GT.grid, BS, 0, E->stream>>>(A, tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x),
@@ -683,7 +739,7 @@ int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
   Q.width = (P.ncols + Q.np - 1) / Q.np;
   const size_t nflat = (size_t)Q.np * P.nrows;
   int* cnt = nullptr;
-  CK(cudaMalloc(&cnt, sizeof(int) * (nflat + 1)));
+  CK(cudaMallocAsync(&cnt, sizeof(int) * (nflat + 1), s));
   CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (nflat + 1), s));
   CK(cudaMalloc(&Q.d_po, sizeof(int) * (nflat + 1)));
   k_panel_count<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width, cnt);
@@ -691,13 +747,13 @@ int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
   size_t tmp_bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, Q.d_po, (int)(nflat + 1), s));
   void* tmp = nullptr;
-  CK(cudaMalloc(&tmp, tmp_bytes));
+  CK(cudaMallocAsync(&tmp, tmp_bytes, s));
   CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, Q.d_po, (int)(nflat + 1), s));
   int total = 0;
   CK(cudaMemcpyAsync(&total, Q.d_po + nflat, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(tmp, s));
+  CK(cudaFreeAsync(cnt, s));
   CK(cudaStreamSynchronize(s));
-  cudaFree(tmp);
-  cudaFree(cnt);
   Q.nnz_short = total;
   CK(cudaMalloc(&Q.d_pci, sizeof(int) * std::max(total, 1)));
   CK(cudaMalloc(&Q.d_pperm, sizeof(int) * std::max(total, 1)));
@@ -875,13 +931,13 @@ int pdcs_transpose_csr(int32_t nrows, int32_t ncols, int32_t nnz, const int32_t*
   cudaStream_t s = (cudaStream_t)stream;
   if (nrows < 0 || ncols < 0 || nnz < 0) { g_err = "pdcs_transpose_csr: bad sizes"; return 2; }
   int* cnt = nullptr;
-  CK(cudaMalloc(&cnt, sizeof(int) * (ncols + 1)));
+  CK(cudaMallocAsync(&cnt, sizeof(int) * (ncols + 1), s));
   CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (ncols + 1), s));
   if (nnz > 0) {
     int *rowid = nullptr, *keys_out = nullptr, *idx = nullptr;
-    CK(cudaMalloc(&rowid, sizeof(int) * nnz));
-    CK(cudaMalloc(&keys_out, sizeof(int) * nnz));
-    CK(cudaMalloc(&idx, sizeof(int) * nnz));
+    CK(cudaMallocAsync(&rowid, sizeof(int) * nnz, s));
+    CK(cudaMallocAsync(&keys_out, sizeof(int) * nnz, s));
+    CK(cudaMallocAsync(&idx, sizeof(int) * nnz, s));
     k_iota_rows<<<grid_for(nrows), BS, 0, s>>>(d_rowptr, nrows, rowid);
     CKL();
     k_iota<<<grid_for(nnz), BS, 0, s>>>(idx, nnz);
@@ -894,25 +950,24 @@ int pdcs_transpose_csr(int32_t nrows, int32_t ncols, int32_t nnz, const int32_t*
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_colidx, keys_out, idx, d_perm, nnz, 0,
                                        bits, s));
     void* tmp = nullptr;
-    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cudaMallocAsync(&tmp, tmp_bytes, s));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, d_colidx, keys_out, idx, d_perm, nnz, 0, bits,
                                        s));
     k_transpose_scatter<<<grid_for(nnz), BS, 0, s>>>(d_perm, rowid, d_val, nnz, d_t_colidx, d_t_val);
     CKL();
-    CK(cudaStreamSynchronize(s));
-    cudaFree(tmp);
-    cudaFree(rowid);
-    cudaFree(keys_out);
-    cudaFree(idx);
+    CK(cudaFreeAsync(tmp, s));
+    CK(cudaFreeAsync(rowid, s));
+    CK(cudaFreeAsync(keys_out, s));
+    CK(cudaFreeAsync(idx, s));
   }
   size_t scan_bytes = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, cnt, d_t_rowptr, ncols + 1, s));
   void* scan_tmp = nullptr;
-  CK(cudaMalloc(&scan_tmp, scan_bytes));
+  CK(cudaMallocAsync(&scan_tmp, scan_bytes, s));
   CK(cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, cnt, d_t_rowptr, ncols + 1, s));
+  CK(cudaFreeAsync(scan_tmp, s));
+  CK(cudaFreeAsync(cnt, s));
   CK(cudaStreamSynchronize(s));
-  cudaFree(scan_tmp);
-  cudaFree(cnt);
   return 0;
 }
 
@@ -983,6 +1038,18 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   cudaStream_t s = E->stream;
   auto fail = [&](int rc) { pdcs_engine_destroy(E); return rc; };
   PhaseTimer T("create", s);
+  {
+    // setup temporaries are stream-ordered allocations (cudaMallocAsync): keep
+    // up to 4 GB of them pooled so a later engine's setup reuses the mapping
+    // (cudaMalloc / cudaFree of the same buffers cost tens of ms and a device sync)
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 4ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
 
   // cone tables: primal blocks start after the box; dual blocks beyond m_elem
   std::vector<PdcsBlock> xb, yb, ux, uy;
@@ -1140,6 +1207,19 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     const int need_t = E->tile_t ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
     E->G.grid = grid_per_sm("gy", need_y, fit(step_y_fn(E), need_y));
     E->GT.grid = grid_per_sm("gt", need_t, fit(step_t_fn(E), need_t));
+    // split step: thread-per-row gather-only passes + streaming epilogues
+    // (single GPU, no chunked long rows, lane-mapped thread-per-row steps);
+    // the epilogue kernels take the step kernels' reduction slots
+    // Measured on C5 (profiles/r02_sweeps.txt): split + hs 704 it/s vs 682 fused
+    // (step_y 0.520 vs 0.555 ms, step_t 0.467 vs 0.506 ms); default on where it applies
+    E->split = tune("split", 1.0) > 0.0 && E->G.n_long == 0 && E->GT.n_long == 0 && !E->tile_y &&
+               !E->tile_t && E->G.step_vw == 1 && E->GT.step_vw == 1 && E->gp == 0 &&
+               E->PG.np > 1 && E->PGT.np > 1;
+    E->hs = tune("hs", 1.0) > 0.0;
+    if (E->split) {
+      E->G.grid = grid_per_sm("gy", grid_for(d.m, BS, 1 << 30), fit((const void*)k_y_epi<false>, grid_for(d.m, BS, 1 << 30)));
+      E->GT.grid = grid_per_sm("gt", grid_for(d.n, BS, 1 << 30), fit((const void*)k_t_epi<false>, grid_for(d.n, BS, 1 << 30)));
+    }
     // the partial-sum passes are latency bound (dependent rowptr -> col ->
     // gather chains): they get every warp slot their registers allow
     const int need_py = grid_for(d.m, BS / E->G.step_vw, 1 << 30);
@@ -1235,10 +1315,11 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   PhaseTimer T("precondition", s);
   int* rowid = nullptr;
   if (nnz > 0) {
-    CK(cudaMalloc(&rowid, sizeof(int) * nnz));
+    CK(cudaMallocAsync(&rowid, sizeof(int) * nnz, s));
     k_iota_rows<<<grid_for(m), BS, 0, s>>>(d.d_g_rowptr, m, rowid);
     CKL();
   }
+  E->precond_mode = enabled;
   // enabled: 0 identity, 1 Ruiz + PC on this matrix, 2 as-is (d1/d2 = cone
   // scales, values untouched), 3 d1/d2 written by the caller (a shard taking
   // the scaling of the full matrix), values scaled by them
@@ -1313,8 +1394,8 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   CKL();
   k_scale_y<<<grid_for(m), BS, 0, s>>>(A, enabled == 2);
   CKL();
+  if (rowid) CK(cudaFreeAsync(rowid, s));
   CK(cudaStreamSynchronize(s));
-  cudaFree(rowid);
   T.lap("ruiz + pc + scale");
   return 0;
 }
@@ -1415,6 +1496,166 @@ int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
     } else {
       stuck = 0;
       last_kbar = hc[b]->k_bar;
+    }
+    b ^= 1;
+  }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+// ---- batched engines: one CUDA graph advances many independent solves ------
+// The graph forks from the batch stream into every member engine's stream
+// (each branch = `slots` line-search trials of that engine, the same launch
+// sequence pdcs_run_inner captures), joins back, and gathers the members'
+// control blocks.  Members whose device loop has stopped are gated off (every
+// step kernel returns on ctrl->stop), so one replay advances exactly the
+// members the host has released; results are bit-identical to running each
+// engine alone.
+struct PdcsBatch {
+  std::vector<Engine*> E;
+  cudaStream_t stream = nullptr;
+  PdcsCtrl** d_src = nullptr;   // [n] member control blocks
+  PdcsCtrl* d_ctrls = nullptr;  // [n] gathered copies
+  PdcsCtrl* h_ctrls = nullptr;  // pinned [2][n]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> join;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int slots = 0;
+  int64_t nodes = 0;
+};
+
+int pdcs_batch_create(PdcsEngine** engines, int32_t n, void* stream, PdcsBatch** out) {
+  if (!engines || n < 1 || !out) { g_err = "pdcs_batch_create: bad arguments"; return 2; }
+  PdcsBatch* B = new PdcsBatch();
+  B->stream = (cudaStream_t)stream;
+  std::vector<PdcsCtrl*> src;
+  for (int i = 0; i < n; ++i) {
+    if (!engines[i] || engines[i]->comm) {
+      delete B;
+      g_err = "pdcs_batch_create: null or sharded engine";
+      return 2;
+    }
+    B->E.push_back(engines[i]);
+    src.push_back(engines[i]->d_ctrl);
+  }
+  B->join.assign(n, nullptr);
+  if (cudaMalloc(&B->d_src, sizeof(PdcsCtrl*) * n) != cudaSuccess ||
+      cudaMalloc(&B->d_ctrls, sizeof(PdcsCtrl) * n) != cudaSuccess ||
+      cudaMallocHost(&B->h_ctrls, sizeof(PdcsCtrl) * 2 * n) != cudaSuccess ||
+      cudaEventCreateWithFlags(&B->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&B->ev[1], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming) != cudaSuccess) {
+    pdcs_batch_destroy(B);
+    g_err = "pdcs_batch_create: allocation failed";
+    return 1;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (cudaEventCreateWithFlags(&B->join[i], cudaEventDisableTiming) != cudaSuccess) {
+      pdcs_batch_destroy(B);
+      g_err = "pdcs_batch_create: event creation failed";
+      return 1;
+    }
+  }
+  if (cudaMemcpyAsync(B->d_src, src.data(), sizeof(PdcsCtrl*) * n, cudaMemcpyHostToDevice, B->stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(B->stream) != cudaSuccess) {
+    pdcs_batch_destroy(B);
+    g_err = "pdcs_batch_create: upload failed";
+    return 1;
+  }
+  *out = B;
+  return 0;
+}
+
+void pdcs_batch_destroy(PdcsBatch* B) {
+  if (!B) return;
+  if (B->stream) cudaStreamSynchronize(B->stream);
+  if (B->exec) cudaGraphExecDestroy(B->exec);
+  if (B->graph) cudaGraphDestroy(B->graph);
+  cudaFree(B->d_src);
+  cudaFree(B->d_ctrls);
+  if (B->h_ctrls) cudaFreeHost(B->h_ctrls);
+  for (auto e : B->ev) if (e) cudaEventDestroy(e);
+  if (B->fork) cudaEventDestroy(B->fork);
+  for (auto e : B->join) if (e) cudaEventDestroy(e);
+  delete B;
+}
+
+static int batch_capture(PdcsBatch* B, int slots) {
+  if (B->exec) { cudaGraphExecDestroy(B->exec); B->exec = nullptr; }
+  if (B->graph) { cudaGraphDestroy(B->graph); B->graph = nullptr; }
+  const int n = (int)B->E.size();
+  cudaStream_t s = B->stream;
+  const int64_t before = g_launches.load();
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  auto abort = [&]() {
+    cudaGraph_t tmp = nullptr;
+    cudaStreamEndCapture(s, &tmp);
+    if (tmp) cudaGraphDestroy(tmp);
+    return 1;
+  };
+  if (cudaEventRecord(B->fork, s) != cudaSuccess) return abort();
+  for (int i = 0; i < n; ++i) {
+    Engine* E = B->E[i];
+    if (cudaStreamWaitEvent(E->stream, B->fork, 0) != cudaSuccess) return abort();
+    for (int k = 0; k < slots; ++k)
+      if (launch_slot(E)) return abort();
+    if (cudaEventRecord(B->join[i], E->stream) != cudaSuccess ||
+        cudaStreamWaitEvent(s, B->join[i], 0) != cudaSuccess)
+      return abort();
+  }
+  k_gather_ctrl<<<grid_for((int64_t)n * (sizeof(PdcsCtrl) / 8)), BS, 0, s>>>(B->d_src, B->d_ctrls, n);
+  if (cudaGetLastError() != cudaSuccess) return abort();
+  CK(cudaStreamEndCapture(s, &B->graph));
+  CK(cudaGraphInstantiate(&B->exec, B->graph, 0));
+  B->nodes = g_launches.load() - before;
+  g_launches.fetch_sub(B->nodes);
+  B->slots = slots;
+  return 0;
+}
+
+int pdcs_batch_run(PdcsBatch* B, int32_t slots) {
+  if (!B) { g_err = "pdcs_batch_run: null batch"; return 2; }
+  if (slots < 1) slots = 1;
+  if (!B->exec || B->slots != slots) {
+    if (batch_capture(B, slots)) return 1;
+  }
+  const int n = (int)B->E.size();
+  cudaStream_t s = B->stream;
+  PdcsCtrl* hc[2] = {B->h_ctrls, B->h_ctrls + n};
+  auto replay = [&](int b) -> int {
+    CK(cudaGraphLaunch(B->exec, s));
+    g_launches.fetch_add(B->nodes);
+    CK(cudaMemcpyAsync(hc[b], B->d_ctrls, sizeof(PdcsCtrl) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(B->ev[b], s));
+    return 0;
+  };
+  // two replays in flight, as in pdcs_run_inner; done when every member's
+  // device loop has stopped; watchdog on the members still running
+  std::vector<int64_t> last(n, -1);
+  int stuck = 0, b = 0;
+  if (replay(0)) return 1;
+  for (;;) {
+    if (replay(b ^ 1)) return 1;
+    CK(cudaEventSynchronize(B->ev[b]));
+    bool all = true, moved = false;
+    for (int i = 0; i < n; ++i) {
+      if (hc[b][i].stop) continue;
+      all = false;
+      if (hc[b][i].k_bar != last[i]) moved = true;
+      last[i] = hc[b][i].k_bar;
+    }
+    if (all) break;
+    if (!moved) {
+      if (++stuck >= 8) {
+        CK(cudaStreamSynchronize(s));
+        g_err = "pdcs_batch_run: device loop made no progress";
+        return 3;
+      }
+    } else {
+      stuck = 0;
     }
     b ^= 1;
   }
@@ -1706,6 +1947,19 @@ int pdcs_comm_unique_id(unsigned char* h_id) {
   ncclUniqueId id;
   CKN(g_nccl.getUniqueId(&id));
   std::memcpy(h_id, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+
+int pdcs_engine_set_uniform_box(PdcsEngine* E, double lo, double hi) {
+  if (!E) { g_err = "pdcs_engine_set_uniform_box: null engine"; return 2; }
+  const char* env = getenv("PDCS_TUNE");
+  if (env && strstr(env, "ubox=0")) return 0;  // measurement switch: read l^, u^ as before
+  E->ubox = true;
+  E->ubox_l = lo;
+  E->ubox_u = hi;
+  if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }  // KArgs are baked into the graph
+  if (E->graph) { cudaGraphDestroy(E->graph); E->graph = nullptr; }
+  E->graph_slots = 0;
   return 0;
 }
 

@@ -124,6 +124,11 @@ struct Engine {
   int gp = 0;  // lane-step gathers: 0 plain, 1 with the L2::64B fill hint
   bool fuse_ctrl = true;  // fold the controllers into the last CTA of the step kernels
   bool pdl = true;        // programmatic dependent launches between the step kernels of a trial
+  bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
+  bool ubox = false;      // every box coordinate has the bounds [ubox_l, ubox_u] (unscaled)
+  double ubox_l = 0.0, ubox_u = 0.0;
+  int precond_mode = 0;   // last pdcs_precondition mode (2 = as-is: bounds unscaled)
+  bool hs = false;        // evict_first L2 policy on the panel passes' streams
   size_t l2_persist = 0;                 // persisting-L2 set-aside requested at create
   int gridY = 1;              // y-space streaming grid (elementwise kernels)
   double* d_partC = nullptr;  // check path partials [max(PDCS_NMET, 4 GAP_K)][capC]

@@ -16,7 +16,29 @@ struct KArgs {
   int* err;
   float keep_xt, keep_yh;  // evict_last fractions of the gathered x~ / y_hat lines
   double* exp_rho;         // per dual exp block: Newton warm starts of its 2 projections (or null)
+  // uniform box (every box coordinate has the same unscaled bounds lu, uu):
+  // ub 1 = the scaled bounds are lu / d2_j, uu / d2_j (exactly k_scale_x's
+  // division), read from d2 -- one stream instead of l^ and u^; ub 2 = as-is
+  // scaling, the bounds are the constants themselves; ub 0 = read l^, u^
+  int ub;
+  double lu, uu;
 };
+
+// Scaled box bounds of coordinate j < nbox (k_scale_x: l^ = l0 / d2).
+template <bool H>
+__device__ __forceinline__ void box_bounds(const KArgs& A, int j, uint64_t ps, double& lj, double& uj) {
+  if (A.ub == 1) {
+    const double dj = ld_hint<H>(A.d2 + j, ps);
+    lj = A.lu / dj;
+    uj = A.uu / dj;
+  } else if (A.ub == 2) {
+    lj = A.lu;
+    uj = A.uu;
+  } else {
+    lj = ld_hint<H>(A.l + j, ps);
+    uj = ld_hint<H>(A.u + j, ps);
+  }
+}
 
 // Controller folded into a step kernel (mode 0 off, 1 line search after the
 // y-step, 2 beta after the G^T step).
@@ -311,6 +333,48 @@ __global__ void k_rowred_long_final(const int* rows, const int* first, int nl, c
 __global__ void k_fill(double* p, int n, double v) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
 }
+// Row-length statistics of a CSR for the SpMV plan (integer sums: exact and
+// order-free, so the atomics are deterministic): [0] sum of short-row
+// lengths, [1] sum of their squares, [2] short rows, [3] long rows (> long_t).
+__global__ void k_row_stats(const int* __restrict__ rp, int nrows, int long_t,
+                            unsigned long long* out) {
+  unsigned long long s1 = 0, s2 = 0, cnt = 0, nl = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x) {
+    const unsigned long long len = (unsigned long long)(rp[r + 1] - rp[r]);
+    if ((long long)len > long_t) {
+      ++nl;
+    } else {
+      s1 += len;
+      s2 += len * len;
+      ++cnt;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    s1 += __shfl_down_sync(0xffffffffu, s1, off);
+    s2 += __shfl_down_sync(0xffffffffu, s2, off);
+    cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    nl += __shfl_down_sync(0xffffffffu, nl, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out + 0, s1);
+    atomicAdd(out + 1, s2);
+    atomicAdd(out + 2, cnt);
+    atomicAdd(out + 3, nl);
+  }
+}
+
+// Long rows (> long_t entries) in ascending order with their [begin, end).
+struct IsLongRow {
+  const int* rp;
+  int long_t;
+  __host__ __device__ bool operator()(int r) const { return rp[r + 1] - rp[r] > long_t; }
+};
+
+__global__ void k_row_extents(const int* __restrict__ rp, const int* rows, int n, int2* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = make_int2(rp[rows[i]], rp[rows[i] + 1]);
+}
+
 __global__ void k_iota_rows(const int* rp, int nrows, int* rowid) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += gridDim.x * blockDim.x)
     for (int j = rp[r]; j < rp[r + 1]; ++j) rowid[j] = r;
@@ -776,7 +840,9 @@ __global__ void __launch_bounds__(BS, 8) k_step_x(KArgs A, double* part, int cap
     const double cj = ld_hint<H>(A.c + j, ps);
     const double v = xn - tau * (cj - gn);
     if (j < A.nbox) {
-      double p = clampv(v, ld_hint<H>(A.l + j, ps), ld_hint<H>(A.u + j, ps));
+      double lj, uj;
+      box_bounds<H>(A, j, ps, lj, uj);
+      double p = clampv(v, lj, uj);
       if (j == 0 && inject) p = __longlong_as_double(0x7ff8000000000000ll);
       st_hint<H>(A.xh + j, p, ps);
       st_hint<H>(A.xt + j, 2.0 * p - xn, pk);
@@ -1075,13 +1141,14 @@ __device__ __forceinline__ void y_epilogue(const KArgs& A, const YCoef& k, int r
 // x-space row j with dot = (G^T y_hat)_j: stores gth and the box part of the
 // dual residual of beta, ||lam1 - P_Lambda lam1||^2, and the bound terms of
 // the dual objective (model.py:182-237, termination.py:113-119).
-template <bool H>
+template <bool H, bool STORE = true>
 __device__ __forceinline__ void t_epilogue(const KArgs& A, int j, double dot, double* acc,
                                            uint64_t ps) {
-  st_hint<H>(A.gth + j, dot, ps);
+  if (STORE) st_hint<H>(A.gth + j, dot, ps);
   if (j < A.nbox) {
     const double lam = ld_hint<H>(A.c + j, ps) - dot;
-    const double lj = ld_hint<H>(A.l + j, ps), uj = ld_hint<H>(A.u + j, ps);
+    double lj, uj;
+    box_bounds<H>(A, j, ps, lj, uj);
     const bool lf = isfinite(lj), uf = isfinite(uj);
     const double pr = (!lf && !uf) ? 0.0 : (!lf ? neg_clip(lam) : (!uf ? pos_part(lam) : lam));
     const double v = lam - pr;
@@ -1142,11 +1209,10 @@ __global__ void __launch_bounds__(BS, 4) k_step_t(KArgs A, TileSrc S, double* pa
 }
 
 // ---- lane-mapped step kernels: VW lanes per row ------------------------------
-template <int VW, int GP>
+template <int VW, int GP, bool H = false>
 __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __restrict__ x,
                                            const double* longv, int r, int sub, int nrows,
                                            uint64_t ps, uint64_t pk) {
-  constexpr bool H = false;
   int b = 0, e = 0;
   double s = 0.0;
   if (r < nrows) {
@@ -1156,7 +1222,7 @@ __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __res
     } else {
       b = ld_hint<H>(S.po + r, ps);
       e = ld_hint<H>(S.po + r + 1, ps);
-      if (S.wpart && sub == 0) s = S.wpart[r];
+      if (S.wpart && sub == 0) s = ld_hint<H>(S.wpart + r, ps);
     }
   }
   if (VW == 1) {
@@ -1191,7 +1257,10 @@ __device__ __forceinline__ double lane_row(const TileSrc& S, const double* __res
   return s;
 }
 
-template <int VW, int GP>
+// HS: the pass's streams (row offsets, entries, partial sums in and out)
+// carry the L2 evict_first policy so the gathered panel stays resident
+// (PDCS_TUNE hs=1; C5 lab: 0.505 vs 0.517 ms per y-step, tools/c5_lab.cu)
+template <int VW, int GP, bool HS = false>
 __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const double* __restrict__ x,
                                                   double* wout, const PdcsCtrl* ctrl, int gate,
                                                   float keep) {
@@ -1204,9 +1273,44 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
   const int wt = gridDim.x * (blockDim.x >> 5);
   for (int base = wg * RPW; base < nrows; base += wt * RPW) {
     const int r = base + lane / VW;
-    const double s = lane_row<VW, GP>(S, x, nullptr, r, sub, nrows, ps, pk);
-    if (sub == 0 && r < nrows) wout[r] = s;
+    const double s = lane_row<VW, GP, HS>(S, x, nullptr, r, sub, nrows, ps, pk);
+    if (sub == 0 && r < nrows) st_hint<HS>(wout + r, s, ps);
   }
+}
+
+// Split step (PDCS_TUNE split=1, matrices without chunked long rows): every
+// panel is a gather-only pass, the last one writing the whole product
+// (G^ x~ into w, G^T y_hat into gth), and the epilogue is a pure stream over
+// the y- (x-) space -- the gathered panel no longer competes in L2 with the
+// 13 epilogue streams (C5 lab: 0.486 vs 0.517 ms per y-step with hs=1).
+template <bool H>
+__global__ void __launch_bounds__(BS, 8) k_y_epi(KArgs A, double* part, int cap, CtrlFuse F) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ YCoef ks;
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
+  const uint64_t ps = policy_stream(), pky = policy_keep_frac(A.keep_yh);
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A.m; r += gridDim.x * blockDim.x)
+    y_epilogue<H>(A, k, r, ld_hint<H>(A.w + r, ps), acc, ps, pky);
+  block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
+}
+
+template <bool H>
+__global__ void __launch_bounds__(BS, 8) k_t_epi(KArgs A, double* part, int cap, CtrlFuse F) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop || !C->accepted) return;
+  const uint64_t ps = policy_stream();
+  double acc[GT_N] = {0.0, 0.0, 0.0};
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.nbox; j += gridDim.x * blockDim.x)
+    t_epilogue<H, false>(A, j, ld_hint<H>(A.gth + j, ps), acc, ps);
+  block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
 }
 
 template <int VW, int GP>
@@ -1517,6 +1621,16 @@ __global__ void k_flush_y(KArgs A) {
   }
 }
 __global__ void k_clear_pending(PdcsCtrl* C) { C->pending = 0; }
+
+// Batched engines: copy every member's control block into one array (one
+// device-to-host copy per batch-graph replay instead of one per engine).
+__global__ void k_gather_ctrl(PdcsCtrl* const* src, PdcsCtrl* dst, int n) {
+  constexpr int W = sizeof(PdcsCtrl) / sizeof(int64_t);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * W; i += gridDim.x * blockDim.x) {
+    const int e = i / W, w = i % W;
+    reinterpret_cast<int64_t*>(dst + e)[w] = reinterpret_cast<const int64_t*>(src[e])[w];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Check path

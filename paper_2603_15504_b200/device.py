@@ -304,6 +304,12 @@ class DeviceEngine:
                 "pdcs_engine_create")
         self.handle = h
         self.asis = asis
+        nb = work.num_box
+        if nb > 0:
+            l0, u0 = np.asarray(work.l[:nb]), np.asarray(work.u[:nb])
+            if np.all(l0 == l0[0]) and np.all(u0 == u0[0]):
+                N.check(lib.pdcs_engine_set_uniform_box(h, float(l0[0]), float(u0[0])),
+                        "pdcs_engine_set_uniform_box")
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(BS, 8) k_xstep(const double* a0, const double*
   if (acc == 12345.0) part[0] = acc;
 }
 
-template <bool FIRST, int MODE = 0>
+template <bool FIRST, int MODE = 0, int GMODE = 0>
 __global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const double* va,
                                              const double* x, const double* win, double* wout) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
@@ -157,9 +157,10 @@ __global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const
       const double v0 = lds<MODE>(va + j);
       const double v1 = q > 1 ? lds<MODE>(va + j + 1) : 0.0, v2 = q > 2 ? lds<MODE>(va + j + 2) : 0.0,
                    v3 = q > 3 ? lds<MODE>(va + j + 3) : 0.0;
-      const double x0 = __ldg(x + c0);
-      const double x1 = q > 1 ? __ldg(x + c1) : 0.0, x2 = q > 2 ? __ldg(x + c2) : 0.0,
-                   x3 = q > 3 ? __ldg(x + c3) : 0.0;
+      const int g0 = GMODE ? r : c0, g1 = GMODE ? r : c1, g2 = GMODE ? r : c2, g3 = GMODE ? r : c3;
+      const double x0 = __ldg(x + g0);
+      const double x1 = q > 1 ? __ldg(x + g1) : 0.0, x2 = q > 2 ? __ldg(x + g2) : 0.0,
+                   x3 = q > 3 ? __ldg(x + g3) : 0.0;
       s += v0 * x0;
       if (q > 1) s += v1 * x1;
       if (q > 2) s += v2 * x2;
@@ -298,24 +299,22 @@ int main(int argc, char** argv) {
   const int gp = occ_pass * nsm, gf = occ_fin * nsm, gx = occ_x * nsm, ge = occ_epi * nsm;
   printf("grids pass %d final %d xstep %d epi %d\n", gp, gf, gx, ge);
 
-  cudaEvent_t e0, e1, e2;
-  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+  cudaEvent_t e0, e1, e2, e3;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
   auto xstep = [&]() {
     k_xstep<<<gx, BS>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6], xs[7], xs[8], xs[9], xs[10], xt, part);
   };
 
-  struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; };
+  struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; int gmode = 0; };
   // fr: panel width fractions; order 0 = panels 0..P-1, 1 = reversed; split: epilogue in its own kernel
   std::vector<Variant> V = {
       {"P3 equal fwd (current)", {1, 1, 1}, 0, 0},
-      {"P3 fwd streams evict_first", {1, 1, 1}, 0, 0, 1},
-      {"P3 fwd streams L1 no_alloc", {1, 1, 1}, 0, 0, 2},
-      {"P4 fwd streams evict_first", {1, 1, 1, 1}, 0, 0, 1},
-      {"P6 fwd streams evict_first", {1, 1, 1, 1, 1, 1}, 0, 0, 1},
       {"P3 split-epi evict_first", {1, 1, 1}, 0, 1, 1},
-      {"P3 equal fwd split-epi", {1, 1, 1}, 0, 1},
-      {"P4 equal fwd", {1, 1, 1, 1}, 0, 0},
-      {"P4 30/30/30/10 fwd", {3, 3, 3, 1}, 0, 0},
+      {"P3 split-epi NO GATHER", {1, 1, 1}, 0, 1, 0, 1},
+      {"P1 split-epi NO GATHER", {1}, 0, 1, 0, 1},
+      {"P1 split-epi gather", {1}, 0, 1, 0, 0},
+      {"P2 split-epi evict_first", {1, 1}, 0, 1, 1},
+      {"P4 split-epi evict_first", {1, 1, 1, 1}, 0, 1, 1},
   };
   for (const Variant& v : V) {
     double tot = 0;
@@ -328,7 +327,7 @@ int main(int argc, char** argv) {
     const int P = Q.P;
     std::vector<int> ord(P);
     for (int i = 0; i < P; ++i) ord[i] = v.order ? P - 1 - i : i;
-    float best = 1e9, sum = 0, xbest = 1e9;
+    float best = 1e9, sum = 0, xbest = 1e9, ebest = 1e9;
     for (int it = 0; it < reps + 2; ++it) {
       CK(cudaEventRecord(e0));
       xstep();
@@ -340,7 +339,10 @@ int main(int argc, char** argv) {
         const int p = ord[i];
         const int* po = Q.d_po + (size_t)p * M;
         double* wo = bufs[i & 1];
-        if (v.mode == 1) {
+        if (v.gmode == 1) {
+          if (i == 0) k_pass<true, 0, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+          else k_pass<false, 0, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        } else if (v.mode == 1) {
           if (i == 0) k_pass<true, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
           else k_pass<false, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
         } else if (v.mode == 2) {
@@ -353,6 +355,7 @@ int main(int argc, char** argv) {
         win = wo;
       }
       if (v.split) {
+        CK(cudaEventRecord(e3));
         k_epi<<<ge, BS>>>(win, Yv, part);
       } else {
         const int p = ord[P - 1];
@@ -362,13 +365,15 @@ int main(int argc, char** argv) {
       }
       CK(cudaEventRecord(e2));
       CK(cudaEventSynchronize(e2));
-      float ms = 0, xms = 0;
+      float ms = 0, xms = 0, ems = 0;
       cudaEventElapsedTime(&xms, e0, e1);
       cudaEventElapsedTime(&ms, e1, e2);
-      if (it >= 2) { best = std::min(best, ms); sum += ms; xbest = std::min(xbest, xms); }
+      if (v.split) cudaEventElapsedTime(&ems, e3, e2);
+      if (it >= 2) { best = std::min(best, ms); sum += ms; xbest = std::min(xbest, xms); ebest = std::min(ebest, ems); }
     }
     CK(cudaGetLastError());
-    printf("%-28s ystep best %.4f ms avg %.4f ms   (xstep %.4f ms)\n", v.name, best, sum / reps, xbest);
+    printf("%-28s ystep best %.4f ms avg %.4f ms   (xstep %.4f ms, epilogue %.4f ms)\n", v.name, best,
+           sum / reps, xbest, v.split ? ebest : 0.0f);
     fflush(stdout);
     free_panels(Q);
   }

@@ -205,6 +205,63 @@ def lp_planted(m=10_000_000, n=20_000_000, nnz_per_row=5, eq_frac=0.3, seed=5) -
                         dual_cones=dual)
 
 
+def entropy_max_primal(nblk=1_000_000, p=1_000, nnz_per_col=4, seed=3) -> ConicProblem:
+    """C3's entropy maximisation with the exponential cones on the PRIMAL side
+    (primal cone blocks at scale): variables per block
+    (t_i, x_i, s_i) in K_exp (s >= x e^{t/x}); ZERO rows A x = b and s_i = 1;
+    minimise -sum t_i, i.e. maximise sum -x_i log x_i.  num_box = 0."""
+    rng = np.random.default_rng(seed)
+    arows = rng.integers(0, p, size=(nblk, nnz_per_col))
+    avals = rng.uniform(0.5, 1.5, size=(nblk, nnz_per_col))
+    acols = np.repeat(np.arange(nblk), nnz_per_col)
+    x0 = rng.uniform(0.1, 1.0, nblk)
+    A = sp.coo_matrix((avals.ravel(), (arows.ravel(), acols)), shape=(p, nblk)).tocsr()
+    A.sum_duplicates()
+    b = A @ x0
+    n, m = 3 * nblk, p + nblk
+    ac = A.tocoo()
+    rows = np.concatenate([ac.row, p + np.arange(nblk)])
+    cols = np.concatenate([3 * ac.col + 1, 3 * np.arange(nblk) + 2])
+    vals = np.concatenate([ac.data, np.ones(nblk)])
+    G = _canon(rows, cols, vals, (m, n))
+    h = np.concatenate([b, np.ones(nblk)])
+    c = np.zeros(n)
+    c[0::3] = -1.0
+    return ConicProblem(c=c, G=G, h=h, l=np.zeros(0), u=np.zeros(0), num_box=0,
+                        primal_cones=tuple(ConeSpec(Cone.EXP, 3) for _ in range(nblk)),
+                        dual_cones=(ConeSpec(Cone.ZERO, m),))
+
+
+def group_regression_primal(ngroups=10_000, gsize=10, q=45_000, nnz_per_row=48, seed=2) -> ConicProblem:
+    """C2's group robust regression with the second-order cones on the PRIMAL
+    side: variables [x (q, free box), then per group (t_g, r_g) in SOC(gsize+1)];
+    ZERO rows A_g x + r_g = b_g; minimise sum t_g.  After Ruiz scaling the
+    primal SOC blocks are non-uniformly scaled, so every projection is the
+    rescaled-SOC root search (cones.py:353-429) -- at scale."""
+    rng = np.random.default_rng(seed)
+    na = ngroups * gsize
+    A = sp.random(na, q, min(1.0, nnz_per_row / q), format="csr", random_state=rng,
+                  data_rvs=rng.standard_normal)
+    x_true = rng.standard_normal(q) * (rng.random(q) < 0.1)
+    bvec = A @ x_true + 0.1 * rng.standard_normal(na)
+    blk = gsize + 1
+    n = q + ngroups * blk
+    ac = A.tocoo()
+    gi, ri = ac.row // gsize, ac.row % gsize
+    # residual variable of row a: r_{g, i} at x-space index q + g*blk + 1 + i
+    rvar = q + np.arange(na) // gsize * blk + 1 + np.arange(na) % gsize
+    rows = np.concatenate([ac.row, np.arange(na)])
+    cols = np.concatenate([ac.col, rvar])
+    vals = np.concatenate([ac.data, np.ones(na)])
+    del gi, ri
+    G = _canon(rows, cols, vals, (na, n))
+    c = np.zeros(n)
+    c[q + np.arange(ngroups) * blk] = 1.0
+    return ConicProblem(c=c, G=G, h=bvec, l=-np.inf * np.ones(q), u=np.inf * np.ones(q), num_box=q,
+                        primal_cones=tuple(ConeSpec(Cone.SOC, blk) for _ in range(ngroups)),
+                        dual_cones=(ConeSpec(Cone.ZERO, na),))
+
+
 CONFIGS = {
     "C1": lambda: lp_random(2000, 4000, 0.01, 0),
     "C2": lambda: group_robust_regression(),

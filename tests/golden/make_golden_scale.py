@@ -10,6 +10,9 @@ Cases (SURVEY.md 8(c) parity contract, VERDICT r1 "next round" item 1):
   c1_1e6, c1_1e4   full C1 (lp_random 2000 x 4000, 1%) to 1e-6 / 1e-4
   c2d_1e4          C2 at 1/10 (1,000 SOC(11) groups, q = 4,500) to 1e-4
   c4d_1e4          C4 at 1/10 (Markowitz RSOC, N = 50,000, k = 40) to 1e-4
+  c3p_1e5, c2p_1e5 small primal-cone instances (exp / rescaled SOC) to 1e-5
+  c3p_traj, c2p_traj  primal-cone instances at scale (100k primal exp blocks,
+                   2,000 primal SOC(11) blocks): the reference's early iterates
   c3h_traj         C3 shape with 100k exponential-cone blocks: the reference's
                    early iterates (k = 5, 10, 20), every 5th coordinate
   c3_traj, c5_traj full-size C3 (1M exp blocks) / C5 (50M nnz): the
@@ -56,6 +59,17 @@ CASES = {
     "c2d_1e4": (lambda: instances.group_robust_regression(ngroups=1000, gsize=10, q=4500,
                                                          nnz_per_row=48, seed=2), TIGHT4, "solve"),
     "c4d_1e4": (lambda: instances.markowitz_rsoc(N=50_000, k=40, seed=4), TIGHT4, "solve"),
+    # primal cone blocks: exp cones and non-uniformly
+    # rescaled SOC blocks on the primal side, solved and traced
+    "c3p_1e5": (lambda: instances.entropy_max_primal(nblk=60, p=8, nnz_per_col=2, seed=3),
+                dict(rel_tol=1e-5, abs_tol=1e-5, time_limit=1e6), "solve"),
+    "c2p_1e5": (lambda: instances.group_regression_primal(ngroups=20, gsize=5, q=60, nnz_per_row=10, seed=2),
+                dict(rel_tol=1e-5, abs_tol=1e-5, time_limit=1e6), "solve"),
+    "c3p_traj": (lambda: instances.entropy_max_primal(nblk=100_000, p=100, nnz_per_col=4, seed=3),
+                 dict(max_iter=20, rel_tol=1e-14, abs_tol=1e-14, time_limit=1e6), "traj"),
+    "c2p_traj": (lambda: instances.group_regression_primal(ngroups=2_000, gsize=10, q=9_000, nnz_per_row=48,
+                                                           seed=2),
+                 dict(max_iter=20, rel_tol=1e-14, abs_tol=1e-14, time_limit=1e6), "traj"),
     "c3h_traj": (lambda: instances.entropy_max(nblk=100_000, p=100, nnz_per_col=4, seed=3),
                  dict(max_iter=20, rel_tol=1e-14, abs_tol=1e-14, time_limit=1e6), "traj"),
     "c3_traj": (lambda: instances.entropy_max(), dict(max_iter=2, rel_tol=1e-14, abs_tol=1e-14,
@@ -63,7 +77,8 @@ CASES = {
     "c5_traj": (lambda: instances.lp_large(), dict(max_iter=3, rel_tol=1e-14, abs_tol=1e-14,
                                                   time_limit=1e6), "traj"),
 }
-TRACE = {"c3h_traj": ((5, 10, 20), 5), "c3_traj": ((1, 2), 50), "c5_traj": ((1, 2, 3), 200)}
+TRACE = {"c3h_traj": ((5, 10, 20), 5), "c3_traj": ((1, 2), 50), "c5_traj": ((1, 2, 3), 200),
+         "c3p_traj": ((5, 10, 20), 5), "c2p_traj": ((5, 10, 20), 1)}
 NOISE_SEEDS = (1, 2, 3)
 
 

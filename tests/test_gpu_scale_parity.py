@@ -12,7 +12,10 @@ Whole solves (SURVEY.md 8(c) contract, no slack factors):
     oracle on both solutions: |e_gpu - e_ref| <= max(1e-6, tol).
 Trajectories: the reference's early iterates (subsampled coordinates) on C3
 with 100k exponential-cone blocks (the warm-started exp-cone Newton at scale),
-on full C3 (1M blocks) and on full C5 (50M nnz).
+on full C3 (1M blocks) and on full C5 (50M nnz), and on primal-cone instances
+at scale: 100k primal exponential-cone blocks and 2,000 primal SOC(11)
+blocks, whose non-uniform scaling makes every projection the rescaled-SOC
+root search (Brent's method on the device).
 """
 
 import json
@@ -55,7 +58,7 @@ def _kkt(p, x, y):
     return np.array([rep["rel_p_inf"], rep["rel_d_inf"], rep["rel_gap_term"]])
 
 
-@pytest.mark.parametrize("name", ["c1_1e6", "c1_1e4", "c2d_1e4", "c4d_1e4"])
+@pytest.mark.parametrize("name", ["c1_1e6", "c1_1e4", "c2d_1e4", "c4d_1e4", "c3p_1e5", "c2p_1e5"])
 def test_solve_matches_reference_at_scale(name):
     import paper_2603_15504_b200 as P
 
@@ -76,7 +79,8 @@ def test_solve_matches_reference_at_scale(name):
     assert np.all(e_gpu <= tol), (name, e_gpu)
 
 
-@pytest.mark.parametrize("name,lim", [("c3h_traj", 1e-10), ("c3_traj", 1e-11), ("c5_traj", 1e-11)])
+@pytest.mark.parametrize("name,lim", [("c3h_traj", 1e-10), ("c3_traj", 1e-11), ("c5_traj", 1e-11),
+                                      ("c3p_traj", 1e-10), ("c2p_traj", 1e-10)])
 def test_trajectory_matches_reference_at_scale(name, lim):
     import paper_2603_15504_b200 as P
 

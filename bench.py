@@ -46,6 +46,11 @@ WORKLOADS = {
            lambda I: I.markowitz_rsoc()),
     "C5": ("C5: lp_large m=10,000,000 n=20,000,000 5 nnz/row (30% ZERO rows, NONNEG rest), box [-2,2]",
            lambda I: I.lp_large()),
+    # primal cone blocks at scale (not BASELINE configurations)
+    "C3p": ("C3p: entropy_max_primal 1M PRIMAL exponential-cone blocks, n=3M m=1.001M",
+            lambda I: I.entropy_max_primal()),
+    "C2p": ("C2p: group_regression_primal 10k PRIMAL SOC(11) blocks (rescaled), n=155k m=100k",
+            lambda I: I.group_regression_primal()),
 }
 
 

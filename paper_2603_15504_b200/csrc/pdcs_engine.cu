@@ -291,7 +291,10 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
 
 // CSR-stream tiles over the short rows (<= TILE_ROWS rows, <= TILE_NNZ
 // entries): only built when the tiled step kernels are chosen.
-int build_tiles(SpmvPlan& P, cudaStream_t s) {
+// head[r] (optional): first row of the cone block holding row r, -1 outside
+// blocks; tiles are then never cut inside a block.  Returns 4 when a block
+// does not fit in one tile (the caller falls back to the unfused y-step).
+int build_tiles(SpmvPlan& P, cudaStream_t s, const std::vector<int>* head = nullptr) {
   const int nrows = P.nrows;
   std::vector<int> rp(nrows + 1, 0);
   if (nrows > 0) {
@@ -300,6 +303,7 @@ int build_tiles(SpmvPlan& P, cudaStream_t s) {
   }
   std::vector<int> tiles(1, 0);
   for (int r = 0; r < nrows;) {
+    const int t0 = r;
     int nz = 0, cnt = 0;
     while (r < nrows && cnt < TILE_ROWS) {
       int len = rp[r + 1] - rp[r];
@@ -308,6 +312,10 @@ int build_tiles(SpmvPlan& P, cudaStream_t s) {
       nz += len;
       ++cnt;
       ++r;
+    }
+    if (head && r < nrows && (*head)[r] >= 0 && (*head)[r] < r) {  // cut inside a block: back up
+      if ((*head)[r] <= t0) return 4;
+      r = (*head)[r];
     }
     tiles.push_back(r);
   }
@@ -565,7 +573,7 @@ int lane_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double* 
 // collective) follows them in the slot.
 CtrlFuse fuse_ls(const Engine* E) {
   CtrlFuse F{};
-  if (E->comm || E->has_yblocks || !E->fuse_ctrl) return F;
+  if (E->comm || (E->has_yblocks && !E->soc_tile) || !E->fuse_ctrl) return F;
   F.mode = 1; F.ticket = E->d_ticket; F.C = E->d_ctrl;
   F.partA = E->d_partX; F.capA = E->capX; F.partB = E->d_partY; F.capB = E->capY;
   F.red = E->d_red; F.err = E->d_err;
@@ -661,8 +669,11 @@ int launch_step_y(Engine* E, const KArgs& A) {
   if (E->split) return E->hs ? split_y<true>(E, A) : split_y<false>(E, A);
   if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
-    k_step_y<<<E->G.grid, BS, 0, E->stream>>>(A, tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y),
-                                             E->d_partY, E->capY, fuse_ls(E));
+    const TileSrc src = tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y);
+    if (E->soc_tile)
+      k_step_y<true><<<E->G.grid, BS, 0, E->stream>>>(A, src, E->d_partY, E->capY, fuse_ls(E), E->d_rowhead);
+    else
+      k_step_y<false><<<E->G.grid, BS, 0, E->stream>>>(A, src, E->d_partY, E->capY, fuse_ls(E), nullptr);
     CKL();
     return 0;
   }
@@ -716,7 +727,7 @@ const void* pass_fn(int vw, int gp) {
 }
 
 const void* step_y_fn(const Engine* E) {
-  if (E->tile_y) return (const void*)k_step_y;
+  if (E->tile_y) return E->soc_tile ? (const void*)k_step_y<true> : (const void*)k_step_y<false>;
   return lane_fn<k_step_y_lane<1, 0>, k_step_y_lane<1, 1>, k_step_y_lane<8, 0>, k_step_y_lane<8, 1>,
                  k_step_y_lane<32, 0>, k_step_y_lane<32, 1>>(E->G.step_vw, E->gp);
 }
@@ -826,9 +837,9 @@ int launch_slot(Engine* E) {
   rc = launch_step_y(E, A);
   if (rc) return 1;
   mark(s, "step_y_spmv");
-  if (E->has_yblocks && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s))
-    return 1;
-  if (E->has_yblocks) mark(s, "blocks_y");
+  const bool yblk = E->has_yblocks && !E->soc_tile;  // else projected inside the tiled y-step
+  if (yblk && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s)) return 1;
+  if (yblk) mark(s, "blocks_y");
   if (E->comm) {
     // sharded: the five y-space and three x-space line-search sums over all
     // ranks (each rank holds a row slice and an x-slice)
@@ -1187,7 +1198,38 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // would be needed
     E->tile_y = tune("tile_y", tune("tile", big * (E->G.step_vw > 1 && E->G.len_cv > 0.5))) > 0.0;
     E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw == 32))) > 0.0;
-    if ((E->tile_y && build_tiles(E->G, s)) || (E->tile_t && build_tiles(E->GT, s))) return fail(1);
+    // dual SOC blocks projected inside the tiled y-step (C2 class): uniform
+    // dual scales, only SOC blocks of at most one tile, no chunked long rows
+    bool soc_tile = E->tile_y && tune("socfuse", 1.0) > 0.0 && !d.allow_nonuniform_dual_soc &&
+                    E->tabY.total() > 0 && E->tabY.n_exp == 0 && E->tabY.n_giant == 0 && E->G.n_long == 0;
+    std::vector<int> head;
+    if (soc_tile) {
+      head.assign(d.m, -1);
+      for (const PdcsBlock& b : yb) {
+        if (b.kind != PDCS_SOC || b.dim > TILE_ROWS) { soc_tile = false; break; }
+        for (int r = b.start; r < b.start + b.dim; ++r) head[r] = b.start;
+      }
+    }
+    if (soc_tile) {
+      const int rc = build_tiles(E->G, s, &head);
+      if (rc == 4) {
+        soc_tile = false;
+        cudaFree(E->G.d_tiles);
+        E->G.d_tiles = nullptr;
+      } else if (rc) {
+        return fail(1);
+      }
+    }
+    if (soc_tile) {
+      if (cudaMalloc(&E->d_rowhead, sizeof(int) * std::max(d.m, 1)) != cudaSuccess ||
+          cudaMemcpyAsync(E->d_rowhead, head.data(), sizeof(int) * d.m, cudaMemcpyHostToDevice, s) !=
+              cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(1);
+      E->soc_tile = true;
+    }
+    if ((E->tile_y && !E->soc_tile && build_tiles(E->G, s)) || (E->tile_t && build_tiles(E->GT, s)))
+      return fail(1);
     T.lap("tiles");
     if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
       return fail(1);
@@ -1288,6 +1330,7 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   free_table(E->tabX);
   free_table(E->tabXs);
   cudaFree(E->d_exp_rho);
+  cudaFree(E->d_rowhead);
   free_table(E->tabY);
   cudaFree(E->d_unif_x);
   cudaFree(E->d_unif_y);

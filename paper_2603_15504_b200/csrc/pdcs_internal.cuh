@@ -125,6 +125,8 @@ struct Engine {
   bool fuse_ctrl = true;  // fold the controllers into the last CTA of the step kernels
   bool pdl = true;        // programmatic dependent launches between the step kernels of a trial
   bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
+  bool soc_tile = false;  // dual SOC blocks projected inside the tiled y-step (d_rowhead)
+  int* d_rowhead = nullptr;  // [m] first row of the cone block of each row, -1 outside
   bool ubox = false;      // every box coordinate has the bounds [ubox_l, ubox_u] (unscaled)
   double ubox_l = 0.0, ubox_u = 0.0;
   int precond_mode = 0;   // last pdcs_precondition mode (2 = as-is: bounds unscaled)

@@ -1170,13 +1170,25 @@ __global__ void __launch_bounds__(BS) k_t_epilogue(KArgs A, double* part, int ca
 }
 
 // ---- tiled (CSR-stream) step kernels -----------------------------------------
+// SOC: the dual SOC blocks (block-uniform scales, each inside one tile: the
+// tiles are cut at block boundaries) are projected here, in the tile, instead
+// of by k_blk_half after the kernel (C2: 10k SOC(11) blocks).  `rowhead[r]` is
+// the first row of row r's block (or -1).  For a block with rows [b, b+d):
+// v = y + sigma (h - w) is projected onto the SOC (the dual kind, cones.py:
+// 436-443), the residual gx_hat - h onto K_d* = SOC (cones.py:523-530) --
+// both plain SOC projections under uniform scales (cones.py:54-67) -- with the
+// norms of the tails summed by the head row's thread in index order.
+template <bool SOC>
 __global__ void __launch_bounds__(BS, 5) k_step_y(KArgs A, TileSrc S, double* part, int cap,
-                                                  CtrlFuse F) {
+                                                  CtrlFuse F, const int* __restrict__ rowhead) {
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
   __shared__ double prod[TILE_NNZ];
   __shared__ int rs[TILE_ROWS + 1];
   __shared__ YCoef ks;  // coefficients in shared memory (register pressure)
+  __shared__ double sv[SOC ? TILE_ROWS : 1], sr[SOC ? TILE_ROWS : 1];
+  // per head row: (mode 0 keep / 1 zero / 2 scale, head value, tail ratio)
+  __shared__ double cv[SOC ? TILE_ROWS : 1][3], cr[SOC ? TILE_ROWS : 1][3];
   if (threadIdx.x == 0) ks = y_coef(C);
   __syncthreads();
   const YCoef& k = ks;
@@ -1184,7 +1196,78 @@ __global__ void __launch_bounds__(BS, 5) k_step_y(KArgs A, TileSrc S, double* pa
   for (int t = blockIdx.x; t < S.ntiles; t += gridDim.x) {
     const int r0 = __ldg(S.tiles + t), nr = __ldg(S.tiles + t + 1) - r0;
     const double dot = tile_rows(S, A.xt, A.w, r0, nr, prod, rs);
-    if (threadIdx.x < nr) y_epilogue<false>(A, k, r0 + threadIdx.x, dot, acc, 0, 0);
+    const int i = threadIdx.x, r = r0 + i;
+    if (!SOC || r >= A.m_elem || i >= nr) {
+      if (i < nr && (!SOC || r < A.m_elem)) y_epilogue<false>(A, k, r, dot, acc, 0, 0);
+    }
+    if (SOC) {
+      // block rows: pending Halpern, pre-projection values into shared memory
+      const bool blk = i < nr && r >= A.m_elem;
+      double yn = 0.0, hi = 0.0, v = 0.0, res = 0.0, gn = 0.0;
+      int head = -1;
+      if (blk) {
+        if (k.pend) {
+          const double yo = A.y[r];
+          yn = k.a * (k.opb * A.yh[r] - k.be * yo) + k.b * A.ya[r];
+          const double go = A.gx[r];
+          gn = k.a * (k.opb * A.gxh[r] - k.be * go) + k.b * A.gxa[r];
+          A.yb[r] = (k.W == 0.0) ? yn : (k.W * A.yb[r] + k.et * yn) / k.tot;
+          A.y[r] = yn;
+          A.gx[r] = gn;
+        } else {
+          yn = A.y[r];
+          gn = A.gx[r];
+        }
+        hi = A.h[r];
+        v = yn + k.sigma * (hi - dot);
+        const double gh = 0.5 * (dot + gn);
+        A.gxh[r] = gh;
+        A.w[r] = dot;
+        res = gh - hi;
+        sv[i] = v;
+        sr[i] = res;
+        head = __ldg(rowhead + r) - r0;
+      }
+      __syncthreads();
+      if (blk && head == i) {
+        // the block's rows are [r, r + d): d from the next head or the tile end
+        int d = 1;
+        while (i + d < nr && __ldg(rowhead + r + d) == r) ++d;
+        double nv = 0.0, nres = 0.0;
+        for (int j = 1; j < d; ++j) {
+          nv += sv[i + j] * sv[i + j];
+          nres += sr[i + j] * sr[i + j];
+        }
+        nv = sqrt(nv);
+        nres = sqrt(nres);
+        const double tv = sv[i], tr = sr[i];
+        // cones.py:54-67: keep if ||x|| <= t, zero if ||x|| <= -t, else
+        // ((t + ||x||)/2) (1, x/||x||) -- the tail as coef/||x|| * x
+        if (nv <= tv) { cv[i][0] = 0.0; } else if (nv <= -tv) { cv[i][0] = 1.0; }
+        else { cv[i][0] = 2.0; cv[i][1] = 0.5 * (tv + nv); cv[i][2] = cv[i][1] / nv; }
+        if (nres <= tr) { cr[i][0] = 0.0; } else if (nres <= -tr) { cr[i][0] = 1.0; }
+        else { cr[i][0] = 2.0; cr[i][1] = 0.5 * (tr + nres); cr[i][2] = cr[i][1] / nres; }
+      }
+      __syncthreads();
+      if (blk) {
+        const double mv = cv[head][0], mr = cr[head][0];
+        double p, rp;
+        if (mv == 0.0) p = v;
+        else if (mv == 1.0) p = 0.0;
+        else p = head == i ? cv[head][1] : cv[head][2] * v;
+        if (mr == 0.0) rp = res;
+        else if (mr == 1.0) rp = 0.0;
+        else rp = head == i ? cr[head][1] : cr[head][2] * res;
+        A.yh[r] = p;
+        const double dy = p - yn;
+        acc[GY_YY] += yn * yn;
+        acc[GY_DYDY] += dy * dy;
+        acc[GY_INTER] += dy * (dot - gn);
+        const double viol = res - rp;
+        acc[GY_RP2] += viol * viol;
+        acc[GY_YH] += p * hi;
+      }
+    }
     __syncthreads();
   }
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);

@@ -604,7 +604,10 @@ int split_passes(Engine* E, const SpmvPlan& P, const PanelPlan& Q, const double*
 template <bool HS>
 int split_y(Engine* E, const KArgs& A) {
   if (split_passes<1, 0, HS>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->d.d_w, 1, E->keep_xt)) return 1;
-  CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
+  if (E->vec && E->m_elem == E->m)
+    CK(launch_step(use_pdl(E), k_y_epi2, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
+  else
+    CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
   CKL();
   return 0;
 }
@@ -612,7 +615,10 @@ int split_y(Engine* E, const KArgs& A) {
 template <bool HS>
 int split_t(Engine* E, const KArgs& A) {
   if (split_passes<1, 0, HS>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->d.d_gth, 2, E->keep_yh)) return 1;
-  CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
+  if (E->vec && E->ubox && E->nbox == E->n)
+    CK(launch_step(use_pdl(E), k_t_epi2, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
+  else
+    CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
   CKL();
   return 0;
 }
@@ -812,8 +818,12 @@ int launch_slot(Engine* E) {
   const KArgs A = make_args(E);
   cudaStream_t s = E->stream;
   BlkParams none{nullptr, nullptr, nullptr, 0, -1};
-  // primal candidate
-  CK(launch_step(use_pdl(E), k_step_x<false>, E->gridStepX, s, A, E->d_partX, E->capX));
+  // primal candidate (pairs of coordinates per 16-byte access when the whole
+  // x-space is one uniform box on one GPU)
+  if (E->vec && E->ubox && E->nbox == E->n && !E->comm && !E->xsplit)
+    CK(launch_step(use_pdl(E), k_step_x2, E->gridStepX2, s, A, E->d_partX, E->capX));
+  else
+    CK(launch_step(use_pdl(E), k_step_x<false>, E->gridStepX, s, A, E->d_partX, E->capX));
   CKL();
   mark(s, "step_x");
   // x-space cone blocks this engine steps (its slice's blocks when sharded)
@@ -1200,7 +1210,9 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     E->tile_t = tune("tile_t", tune("tile", big * (E->GT.step_vw == 32))) > 0.0;
     // dual SOC blocks projected inside the tiled y-step (C2 class): uniform
     // dual scales, only SOC blocks of at most one tile, no chunked long rows
-    bool soc_tile = E->tile_y && tune("socfuse", 1.0) > 0.0 && !d.allow_nonuniform_dual_soc &&
+    // Opt-in (PDCS_TUNE socfuse=1): measured equal on C2 (8704 vs 8701 it/s; the fused
+    // k_step_y<1> takes 70 us against 43 + 22 + 12 us unfused), profiles/r02_sweeps.txt
+    bool soc_tile = E->tile_y && tune("socfuse", 0.0) > 0.0 && !d.allow_nonuniform_dual_soc &&
                     E->tabY.total() > 0 && E->tabY.n_exp == 0 && E->tabY.n_giant == 0 && E->G.n_long == 0;
     std::vector<int> head;
     if (soc_tile) {
@@ -1245,6 +1257,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       return per > 0 ? std::max(1, std::min(needed, per * nsm)) : dflt;
     };
     E->gridStepX = grid_per_sm("gx", E->gridX, fit((const void*)k_step_x<false>, E->gridX));
+    E->gridStepX2 = std::min(E->gridStepX, fit((const void*)k_step_x2, grid_for(d.n / 2 + 1)));
     const int need_y = E->tile_y ? std::max(1, E->G.ntiles) : grid_for(d.m, BS / E->G.step_vw, 1 << 30);
     const int need_t = E->tile_t ? std::max(1, E->GT.ntiles) : grid_for(d.n, BS / E->GT.step_vw, 1 << 30);
     E->G.grid = grid_per_sm("gy", need_y, fit(step_y_fn(E), need_y));
@@ -1258,9 +1271,15 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
                !E->tile_t && E->G.step_vw == 1 && E->GT.step_vw == 1 && E->gp == 0 &&
                E->PG.np > 1 && E->PGT.np > 1;
     E->hs = tune("hs", 1.0) > 0.0;
+    E->vec = tune("vec", 1.0) > 0.0;  // double2 streaming epilogues (split step only)
     if (E->split) {
-      E->G.grid = grid_per_sm("gy", grid_for(d.m, BS, 1 << 30), fit((const void*)k_y_epi<false>, grid_for(d.m, BS, 1 << 30)));
-      E->GT.grid = grid_per_sm("gt", grid_for(d.n, BS, 1 << 30), fit((const void*)k_t_epi<false>, grid_for(d.n, BS, 1 << 30)));
+      const void* ye = (E->vec && d.m_elem == d.m) ? (const void*)k_y_epi2 : (const void*)k_y_epi<false>;
+      // one wave of the epilogue kernel that will run (k_t_epi2 also needs the uniform box,
+      // known after create; without it k_t_epi runs on the same grid)
+      const int ny = grid_for(d.m, BS, 1 << 30), nx = grid_for(d.n, BS, 1 << 30);
+      E->G.grid = grid_per_sm("gy", ny, fit(ye, ny));
+      E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
+                                                : fit((const void*)k_t_epi<false>, nx));
     }
     // the partial-sum passes are latency bound (dependent rowptr -> col ->
     // gather chains): they get every warp slot their registers allow

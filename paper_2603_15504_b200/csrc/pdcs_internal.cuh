@@ -119,6 +119,7 @@ struct Engine {
   int capX = 0, capY = 0, capT = 0;
   int gridX = 1, gridXE = 1;  // x-space streaming grid
   int gridStepX = 1;          // k_step_x grid (one wave of resident CTAs)
+  int gridStepX2 = 1;         // k_step_x2 grid (16-byte variant)
   float keep_xt = 1.0f, keep_yh = 1.0f;  // evict_last fractions (L2 set-aside / vector bytes)
   bool tile_y = false, tile_t = false;  // step SpMVs: tiled CSR-stream or lane-mapped
   int gp = 0;  // lane-step gathers: 0 plain, 1 with the L2::64B fill hint
@@ -126,6 +127,7 @@ struct Engine {
   bool pdl = true;        // programmatic dependent launches between the step kernels of a trial
   bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
   bool soc_tile = false;  // dual SOC blocks projected inside the tiled y-step (d_rowhead)
+  bool vec = false;       // 16-byte streaming epilogues of the split step
   int* d_rowhead = nullptr;  // [m] first row of the cone block of each row, -1 outside
   bool ubox = false;      // every box coordinate has the bounds [ubox_l, ubox_u] (unscaled)
   double ubox_l = 0.0, ubox_u = 0.0;

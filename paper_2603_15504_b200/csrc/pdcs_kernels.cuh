@@ -1361,6 +1361,233 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
   }
 }
 
+// ---- 16-byte (double2) streaming variants of the step epilogues -------------
+// The same per-element arithmetic as k_step_x / y_epilogue / t_epilogue, with
+// every stream moved as aligned pairs (one 16-byte load or store per two
+// elements): twice the bytes in flight per instruction for the HBM-bound
+// streams.  Used when every row is elementwise (no cone blocks in the space);
+// odd lengths finish with one scalar element.
+__device__ __forceinline__ double2 ld2(const double* p, int i) {
+  return __ldg(reinterpret_cast<const double2*>(p) + i);
+}
+__device__ __forceinline__ double2 ldc2(const double* p, int i) {
+  return reinterpret_cast<const double2*>(p)[i];
+}
+__device__ __forceinline__ void st2(double* p, int i, double a, double b) {
+  reinterpret_cast<double2*>(p)[i] = make_double2(a, b);
+}
+
+// y-space row r (elementwise block) with dot = (G^ x~)_r and the loaded operands
+__device__ __forceinline__ void y_elem(const KArgs& A, const YCoef& k, int r, double dot, double y,
+                                       double yh, double ya, double yb, double gx, double gxh,
+                                       double gxa, double hi, double& o_y, double& o_yb, double& o_gx,
+                                       double& o_gxh, double& o_yh, double* acc) {
+  double yn, gn;
+  if (k.pend) {
+    yn = k.a * (k.opb * yh - k.be * y) + k.b * ya;
+    gn = k.a * (k.opb * gxh - k.be * gx) + k.b * gxa;
+    o_yb = (k.W == 0.0) ? yn : (k.W * yb + k.et * yn) / k.tot;
+  } else {
+    yn = y;
+    gn = gx;
+    o_yb = yb;
+  }
+  o_y = yn;
+  o_gx = gn;
+  const double v = yn + k.sigma * (hi - dot);
+  const double gh = 0.5 * (dot + gn);
+  o_gxh = gh;
+  const bool zero = r < A.m_zero;
+  const double p = zero ? v : pos_part(v);
+  o_yh = p;
+  const double dy = p - yn;
+  acc[GY_YY] += yn * yn;
+  acc[GY_DYDY] += dy * dy;
+  acc[GY_INTER] += dy * (dot - gn);
+  const double res = gh - hi;
+  const double viol = zero ? res : res - pos_part(res);
+  acc[GY_RP2] += viol * viol;
+  acc[GY_YH] += p * hi;
+}
+
+__global__ void __launch_bounds__(BS, 4) k_y_epi2(KArgs A, double* part, int cap, CtrlFuse F) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ YCoef ks;
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int np = A.m >> 1;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int q = tid; q < np; q += nt) {
+    const double2 w = ldc2(A.w, q), y = ldc2(A.y, q), yh = ldc2(A.yh, q), ya = ld2(A.ya, q),
+                  yb = ldc2(A.yb, q), gx = ldc2(A.gx, q), gxh = ldc2(A.gxh, q), gxa = ld2(A.gxa, q),
+                  h = ld2(A.h, q);
+    double oy0, oyb0, ogx0, ogxh0, oyh0, oy1, oyb1, ogx1, ogxh1, oyh1;
+    y_elem(A, k, 2 * q, w.x, y.x, yh.x, ya.x, yb.x, gx.x, gxh.x, gxa.x, h.x, oy0, oyb0, ogx0, ogxh0, oyh0, acc);
+    y_elem(A, k, 2 * q + 1, w.y, y.y, yh.y, ya.y, yb.y, gx.y, gxh.y, gxa.y, h.y, oy1, oyb1, ogx1, ogxh1, oyh1,
+           acc);
+    if (k.pend) {
+      st2(A.y, q, oy0, oy1);
+      st2(A.yb, q, oyb0, oyb1);
+      st2(A.gx, q, ogx0, ogx1);
+    }
+    st2(A.gxh, q, ogxh0, ogxh1);
+    st2(A.yh, q, oyh0, oyh1);
+  }
+  if ((A.m & 1) && tid == 0) {
+    const int r = A.m - 1;
+    double oy, oyb, ogx, ogxh, oyh;
+    y_elem(A, k, r, A.w[r], A.y[r], A.yh[r], A.ya[r], A.yb[r], A.gx[r], A.gxh[r], A.gxa[r], A.h[r], oy, oyb,
+           ogx, ogxh, oyh, acc);
+    if (k.pend) {
+      A.y[r] = oy;
+      A.yb[r] = oyb;
+      A.gx[r] = ogx;
+    }
+    A.gxh[r] = ogxh;
+    A.yh[r] = oyh;
+  }
+  block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
+}
+
+// x-space coordinate j of k_step_x (box-only, uniform box) with loaded operands
+__device__ __forceinline__ void x_elem(const KArgs& A, bool pend, bool inject, const double* kc, double x,
+                                       double xh, double xa, double xb, double gty, double gth,
+                                       double gtya, double cj, double dj, double& o_x, double& o_xb,
+                                       double& o_gty, double& o_xh, double& o_xt, double* acc) {
+  const double &a = kc[0], &b = kc[1], &be = kc[2], &et = kc[3], &W = kc[4], &tau = kc[5];
+  const double &opb = kc[6], &tot = kc[7];
+  double xn, gn;
+  if (pend) {
+    xn = a * (opb * xh - be * x) + b * xa;
+    gn = a * (opb * gth - be * gty) + b * gtya;
+    o_xb = (W == 0.0) ? xn : (W * xb + et * xn) / tot;
+  } else {
+    xn = x;
+    gn = gty;
+    o_xb = xb;
+  }
+  o_x = xn;
+  o_gty = gn;
+  const double v = xn - tau * (cj - gn);
+  double lj, uj;
+  if (A.ub == 2) {
+    lj = A.lu;
+    uj = A.uu;
+  } else {
+    lj = A.lu / dj;
+    uj = A.uu / dj;
+  }
+  double p = clampv(v, lj, uj);
+  if (inject) p = __longlong_as_double(0x7ff8000000000000ll);  // debug NaN hook (coordinate 0)
+  o_xh = p;
+  o_xt = 2.0 * p - xn;
+  const double d = p - xn;
+  acc[GX_XX] += xn * xn;
+  acc[GX_DXDX] += d * d;
+  acc[GX_CX] += cj * p;
+}
+
+// k_step_x over a uniform box covering all of x-space (single GPU, no NaN
+// injection), pairs of coordinates per 16-byte access
+__global__ void __launch_bounds__(BS, 4) k_step_x2(KArgs A, double* part, int cap) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ double kc[8];
+  if (threadIdx.x == 0) {
+    kc[0] = C->pa; kc[1] = C->pb; kc[2] = C->pbeta; kc[3] = C->peta; kc[4] = C->pW; kc[5] = C->tau;
+    kc[6] = 1.0 + C->pbeta; kc[7] = C->pW + C->peta;
+  }
+  __syncthreads();
+  const bool pend = C->pending != 0;
+  const bool inject = C->nan_after >= 0 && C->n_primal_proj >= C->nan_after;
+  double acc[GX_N] = {0.0, 0.0, 0.0};
+  const int np = A.n >> 1;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int q = tid; q < np; q += nt) {
+    const double2 x = ldc2(A.x, q), gty = ldc2(A.gty, q), c = ld2(A.c, q);
+    const double2 d = A.ub == 1 ? ld2(A.d2, q) : make_double2(1.0, 1.0);
+    double2 xh, xa, xb, gth, gtya;
+    if (pend) {
+      xh = ldc2(A.xh, q); xa = ld2(A.xa, q); xb = ldc2(A.xb, q); gth = ldc2(A.gth, q); gtya = ld2(A.gtya, q);
+    } else {
+      xh = xa = xb = gth = gtya = make_double2(0.0, 0.0);
+    }
+    double ox0, oxb0, og0, oxh0, oxt0, ox1, oxb1, og1, oxh1, oxt1;
+    x_elem(A, pend, inject && q == 0, kc, x.x, xh.x, xa.x, xb.x, gty.x, gth.x, gtya.x, c.x, d.x, ox0, oxb0, og0,
+           oxh0, oxt0, acc);
+    x_elem(A, pend, false, kc, x.y, xh.y, xa.y, xb.y, gty.y, gth.y, gtya.y, c.y, d.y, ox1, oxb1, og1, oxh1, oxt1,
+           acc);
+    if (pend) {
+      st2(A.xb, q, oxb0, oxb1);
+      st2(A.x, q, ox0, ox1);
+      st2(A.gty, q, og0, og1);
+    }
+    st2(A.xh, q, oxh0, oxh1);
+    st2(A.xt, q, oxt0, oxt1);
+  }
+  if ((A.n & 1) && tid == 0) {
+    const int j = A.n - 1;
+    double ox, oxb, og, oxh, oxt;
+    x_elem(A, pend, inject && j == 0, kc, A.x[j], A.xh[j], A.xa[j], A.xb[j], A.gty[j], A.gth[j], A.gtya[j],
+           A.c[j], A.ub == 1 ? A.d2[j] : 1.0, ox, oxb, og, oxh, oxt, acc);
+    if (pend) {
+      A.xb[j] = oxb;
+      A.x[j] = ox;
+      A.gty[j] = og;
+    }
+    A.xh[j] = oxh;
+    A.xt[j] = oxt;
+  }
+  block_store_mask<GX_N>(acc, 0u, part, cap, blockIdx.x);
+}
+
+// x-space box coordinate j with dot = (G^T y_hat)_j (t_epilogue without the store)
+__device__ __forceinline__ void t_elem(const KArgs& A, double dot, double cj, double dj, double* acc) {
+  double lj, uj;
+  if (A.ub == 2) {
+    lj = A.lu;
+    uj = A.uu;
+  } else {
+    lj = A.lu / dj;
+    uj = A.uu / dj;
+  }
+  const double lam = cj - dot;
+  const bool lf = isfinite(lj), uf = isfinite(uj);
+  const double pr = (!lf && !uf) ? 0.0 : (!lf ? neg_clip(lam) : (!uf ? pos_part(lam) : lam));
+  const double v = lam - pr;
+  acc[GT_RD2] += v * v;
+  if (lf) acc[GT_LSUM] += lj * pos_part(lam);
+  if (uf) acc[GT_USUM] += uj * pos_part(-lam);
+}
+
+// needs a uniform box over all of x-space (ub != 0, nbox == n)
+__global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap, CtrlFuse F) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop || !C->accepted) return;
+  double acc[GT_N] = {0.0, 0.0, 0.0};
+  const int np = A.nbox >> 1;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int q = tid; q < np; q += nt) {
+    const double2 g = ldc2(A.gth, q), c = ld2(A.c, q);
+    const double2 d = A.ub == 1 ? ld2(A.d2, q) : make_double2(1.0, 1.0);
+    t_elem(A, g.x, c.x, d.x, acc);
+    t_elem(A, g.y, c.y, d.y, acc);
+  }
+  if ((A.nbox & 1) && tid == 0) {
+    const int j = A.nbox - 1;
+    t_elem(A, A.gth[j], A.c[j], A.ub == 1 ? A.d2[j] : 1.0, acc);
+  }
+  block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
+  fused_ctrl(F);
+}
+
 // Split step (PDCS_TUNE split=1, matrices without chunked long rows): every
 // panel is a gather-only pass, the last one writing the whole product
 // (G^ x~ into w, G^T y_hat into gth), and the epilogue is a pure stream over

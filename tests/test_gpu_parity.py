@@ -167,6 +167,20 @@ def _kkt_triplet(p, x, y):
     return np.array([rep["rel_p_inf"], rep["rel_d_inf"], rep["rel_gap_term"]])
 
 
+def _bands():
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "noise_bands.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        return {k: tuple(v) for k, v in json.load(f).items()}
+
+
+_BANDS = _bands()
+
+
 @pytest.mark.parametrize("case", SOLVE_CASES)
 def test_solve_matches_reference(P, case):
     d = load("solve_" + case)
@@ -185,8 +199,11 @@ def test_solve_matches_reference(P, case):
     assert r.exit_status == status, (case, r.exit_status, status, r.iterations)
     ref_it = int(d["iterations"])
     freq = opts.get("duality_gap_restart_freq", 2000)
-    band = max(int(0.2 * ref_it), freq)
-    assert abs(r.iterations - ref_it) <= band, (case, r.iterations, ref_it)
+    # the reference's own band under 1-ulp SpMV noise (tests/golden/noise_bands.json,
+    # make_noise_bands.py: 6 noise seeds), widened by one check interval
+    nominal, lo, hi = _BANDS.get(case, (ref_it, ref_it, ref_it))
+    assert nominal == ref_it
+    assert lo - freq <= r.iterations <= hi + freq, (case, r.iterations, (lo, hi))
     tol = max(opts.get("rel_tol", 1e-6), 1e-6)
     if status == ":optimal":
         p_ref = float(d["p_obj"])

@@ -398,14 +398,20 @@ __device__ __forceinline__ bool exp_cheap(double r, double s, double t, double* 
     o[0] = r; o[1] = s; o[2] = t;
     return true;
   }
-  if (exp_member(r, s, t)) { o[0] = r; o[1] = s; o[2] = t; return true; }
+  // exp(r/s) serves both the membership test (cones.py:80-88) and the primal
+  // heuristic (cones.py:102-113): computed once (the same operations, so the
+  // same bits as computing it twice)
+  const double ers = s > 0.0 ? exp_guard(r / s) : 0.0;
+  const bool member = s > 0.0 ? (r / s < 709.0 && t >= 0.0 && t >= s * ers)
+                              : ((s >= 0.0 && s <= 0.0) && r <= 0.0 && t >= 0.0);
+  if (member) { o[0] = r; o[1] = s; o[2] = t; return true; }
   if (dual_exp_member(-r, -s, -t)) { o[0] = 0.0; o[1] = 0.0; o[2] = 0.0; return true; }
   if (r <= 0.0 && s <= 0.0) { o[0] = r; o[1] = 0.0; o[2] = t < 0.0 ? 0.0 : t; return true; }
   // primal heuristic (cones.py:102-113)
   double vp0 = dmin(r, 0.0), vp1 = 0.0, vp2 = dmax(t, 0.0);
   double pdist = sqrt((r - vp0) * (r - vp0) + s * s + (t - vp2) * (t - vp2));
   if (s > 0.0) {
-    double tp = s * exp_guard(r / s);
+    double tp = s * ers;
     if (isfinite(tp)) {
       tp = dmax(t, tp);
       if (tp - t < pdist) { vp0 = r; vp1 = s; vp2 = tp; pdist = tp - t; }

@@ -452,7 +452,13 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
     CKL();
     slot += T.g_exp;
   } else if (T.n_exp) {
-    k_blk_exp<OP><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
+    // PDCS_TUNE expminb=2|3: more registers per thread for the (FP64-bound) y-step exp blocks
+    if (OP == OP_STEP_Y && T.exp_minb == 2)
+      k_blk_exp<OP, 2><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
+    else if (OP == OP_STEP_Y && T.exp_minb == 3)
+      k_blk_exp<OP, 3><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
+    else
+      k_blk_exp<OP><<<T.g_exp, BS, 0, s>>>(base, T.n_exp, A, P, part, cap, slot, gate);
     CKL();
   }
   slot += T.g_exp;
@@ -1109,11 +1115,11 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     // one kernel, 2.27-2.41k vs 2.75k it/s; profiles/r02_sweeps.txt)
     const char* env = getenv("PDCS_TUNE");
     const bool on = env && (strstr(env, "expsplit=1") != nullptr);
+    const char* mb = env ? strstr(env, "expminb=") : nullptr;
+    E->tabY.exp_minb = mb ? atoi(mb + 8) : 4;
     if (on) {
       BlockTable& T = E->tabY;
       T.exp_split = true;
-      const char* mb = env ? strstr(env, "expminb=") : nullptr;
-      if (mb) T.exp_minb = atoi(mb + 8);
       T.exp_per = (T.n_exp + T.g_exp - 1) / T.g_exp;
       if (cudaMalloc(&T.d_queue, sizeof(int) * T.n_exp) != cudaSuccess ||
           cudaMalloc(&T.d_qcount, sizeof(int) * T.g_exp) != cudaSuccess)

@@ -63,7 +63,7 @@ struct BlockTable {
   // needing the root search at d_queue[c*exp_per ...], d_qcount[c] of them
   bool exp_split = false;
   int exp_per = 0;
-  int exp_minb = 2;  // CTAs per SM the fast kernel is compiled for (register budget)
+  int exp_minb = 4;  // CTAs per SM the exp kernels are compiled for (register budget; PDCS_TUNE expminb)
   int* d_queue = nullptr;   // [n_exp]
   int* d_qcount = nullptr;  // [g_exp]
   int total() const { return n_exp + n_thread + n_half + n_warp + n_cta + n_giant; }

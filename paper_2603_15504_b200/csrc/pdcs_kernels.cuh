@@ -559,8 +559,8 @@ __device__ __forceinline__ bool exp_or_dual_fast(int kind, const double* v, doub
   return proj_dual_exp3_fast(v[0], v[1], v[2], o, err, rho);
 }
 
-template <int OP>
-__global__ void __launch_bounds__(BS, 4) k_blk_exp(const PdcsBlock* tab, int nb, KArgs A, BlkParams P,
+template <int OP, int MINB = 4>
+__global__ void __launch_bounds__(BS, MINB) k_blk_exp(const PdcsBlock* tab, int nb, KArgs A, BlkParams P,
                                                 double* part, int cap, int slot0, int gate) {
   if (gated(A.ctrl, gate)) return;
   constexpr int NQ = OpNQ<OP>::v;

@@ -77,9 +77,12 @@ __device__ __forceinline__ int ld_hint(const int* a, uint64_t pol) {
 }
 // Gather load with an explicit L2 fill size: GP = 0 plain, 1 = 64 B, 2 = 128 B
 // (random 8-byte gathers otherwise pull larger lines from HBM).
+// GP 3: coherent L2 load (ld.global.cg) for a vector the same kernel writes
+// (the persistent trial kernel gathers x~ / y_hat produced by other CTAs)
 template <int GP>
 __device__ __forceinline__ double ld_gather(const double* a) {
   if (GP == 0) return __ldg(a);
+  if (GP == 3) return __ldcg(a);
   double v;
   if (GP == 1) asm("ld.global.nc.L2::64B.f64 %0, [%1];" : "=d"(v) : "l"(a));
   else asm("ld.global.nc.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(a));

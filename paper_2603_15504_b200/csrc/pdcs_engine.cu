@@ -1304,6 +1304,28 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     E->keep_yh = (float)tune("keep_yh", 1.0);
     cudaGetLastError();
   }
+  {
+    // persistent trials (k_persist) for small block-free instances on one GPU:
+    // C1 class (launch-latency bound); PDCS_TUNE persist=0 keeps the graph path
+    const char* env = getenv("PDCS_TUNE");
+    const bool off = env && strstr(env, "persist=0");
+    const bool vw_ok = [](int v) { return v == 1 || v == 8 || v == 32; }(E->G.step_vw) &&
+                       [](int v) { return v == 1 || v == 8 || v == 32; }(E->GT.step_vw);
+    int coop = 0, dev = 0, nsm = NSM;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (!off && coop && vw_ok && !E->has_xblocks && !E->has_yblocks && E->G.n_long == 0 &&
+        E->GT.n_long == 0 && E->PG.np == 1 && E->PGT.np == 1 && !E->tile_y && !E->tile_t && !E->split &&
+        d.nnz <= (1 << 22) && d.n > 0 && d.m > 0) {
+      E->pgrid = nsm;
+      if (cudaMalloc(&E->d_pX, sizeof(double) * GX_N * E->pgrid) == cudaSuccess &&
+          cudaMalloc(&E->d_pY, sizeof(double) * GY_N * E->pgrid) == cudaSuccess &&
+          cudaMalloc(&E->d_pT, sizeof(double) * GT_N * E->pgrid) == cudaSuccess)
+        E->persist = true;
+      cudaGetLastError();
+    }
+  }
   E->capX = E->gridStepX + E->tabX.grids();
   E->capY = E->G.grid + E->tabY.grids();
   E->capT = E->GT.grid + E->tabX.grids();
@@ -1356,6 +1378,9 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   free_table(E->tabXs);
   cudaFree(E->d_exp_rho);
   cudaFree(E->d_rowhead);
+  cudaFree(E->d_pX);
+  cudaFree(E->d_pY);
+  cudaFree(E->d_pT);
   free_table(E->tabY);
   cudaFree(E->d_unif_x);
   cudaFree(E->d_unif_y);
@@ -1508,8 +1533,51 @@ int pdcs_engine_set_ctrl(PdcsEngine* E, const PdcsCtrl* h) {
   return 0;
 }
 
+extern "C++" {
+template <int VWY, int VWT>
+static int persist_launch(Engine* E, long long max_trials) {
+  KArgs A = make_args(E);
+  TileSrc SY = tile_source(E->G, E->PG, 0, nullptr), ST = tile_source(E->GT, E->PGT, 0, nullptr);
+  double *pX = E->d_pX, *pY = E->d_pY, *pT = E->d_pT;
+  int cap = E->pgrid;
+  void* args[] = {&A, &SY, &ST, &pX, &pY, &pT, &cap, &max_trials};
+  CK(cudaLaunchCooperativeKernel((const void*)k_persist<VWY, VWT>, E->pgrid, BS, args, 0, E->stream));
+  g_launches.fetch_add(1);
+  return 0;
+}
+
+// The device loop of a persistent engine: one cooperative launch until the
+// control block stops (batch end, check, budget, error).  The trial cap only
+// guards against a hang: 61 trials per remaining iteration (60 rejections
+// trip the trial cap) plus slack.
+static int run_persist(Engine* E) {
+  PdcsCtrl c;
+  CK(cudaMemcpyAsync(E->h_pinned, E->d_ctrl, sizeof(PdcsCtrl), cudaMemcpyDeviceToHost, E->stream));
+  CK(cudaStreamSynchronize(E->stream));
+  std::memcpy(&c, E->h_pinned, sizeof(PdcsCtrl));
+  const long long left = std::max<long long>(1, std::min<long long>(c.k_bar_stop, c.max_iter) - c.k_bar);
+  const long long max_trials = left * 61 + 128;
+  int rc = 0;
+  switch (E->G.step_vw * 100 + E->GT.step_vw) {
+    case 101: rc = persist_launch<1, 1>(E, max_trials); break;
+    case 108: rc = persist_launch<1, 8>(E, max_trials); break;
+    case 132: rc = persist_launch<1, 32>(E, max_trials); break;
+    case 801: rc = persist_launch<8, 1>(E, max_trials); break;
+    case 808: rc = persist_launch<8, 8>(E, max_trials); break;
+    case 832: rc = persist_launch<8, 32>(E, max_trials); break;
+    case 3201: rc = persist_launch<32, 1>(E, max_trials); break;
+    case 3208: rc = persist_launch<32, 8>(E, max_trials); break;
+    default: rc = persist_launch<32, 32>(E, max_trials); break;
+  }
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(E->stream));
+  return 0;
+}
+}  // extern "C++"
+
 int pdcs_run_inner(PdcsEngine* E, int32_t slots) {
   if (slots < 1) slots = 1;
+  if (E->persist && !E->comm) return run_persist(E);
   cudaStream_t s = E->stream;
   if (!E->exec || E->graph_slots != slots) {
     if (E->exec) { cudaGraphExecDestroy(E->exec); E->exec = nullptr; }

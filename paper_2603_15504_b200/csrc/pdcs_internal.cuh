@@ -128,6 +128,9 @@ struct Engine {
   bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
   bool soc_tile = false;  // dual SOC blocks projected inside the tiled y-step (d_rowhead)
   bool vec = false;       // 16-byte streaming epilogues of the split step
+  bool persist = false;   // small instances: one cooperative launch runs all trials (k_persist)
+  int pgrid = 0;          // its grid (one CTA per SM)
+  double *d_pX = nullptr, *d_pY = nullptr, *d_pT = nullptr;  // its partial slots [NQ][pgrid]
   int* d_rowhead = nullptr;  // [m] first row of the cone block of each row, -1 outside
   bool ubox = false;      // every box coordinate has the bounds [ubox_l, ubox_u] (unscaled)
   double ubox_l = 0.0, ubox_u = 0.0;

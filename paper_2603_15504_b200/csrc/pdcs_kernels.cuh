@@ -1,5 +1,7 @@
 // Kernels of libpdcs.  Included by pdcs_engine.cu only.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "pdcs_internal.cuh"
 
 namespace pdcs {
@@ -2260,6 +2262,120 @@ __global__ void k_unscale(KArgs A, const double* x, const double* y, const doubl
     const double d = A.d1[i];
     yo[i] = y[i] * d;
     slack[i] = gx[i] / d - A.h0[i];
+  }
+}
+
+}  // namespace pdcs
+
+namespace pdcs {
+
+// ---------------------------------------------------------------------------
+// Persistent trials for small instances (C1 class: thousands of rows, no cone
+// blocks, one column panel).  A trial of the graph path is three ~8 us
+// kernels bound by launch and grid-drain latency; here ONE cooperative launch
+// (one CTA per SM) runs every trial up to the batch end with grid-wide
+// barriers between the phases:
+//   X (primal step) | sync | Y (G^ x~ + dual step) | sync | line search |
+//   [accepted] T (G^T y_hat + beta partials) | sync | beta
+// Every CTA keeps an identical copy of the control block in shared memory and
+// runs both controllers redundantly on the same partial sums read in the same
+// order (bit-identical decisions, no extra barrier); CTA 0 writes it back at
+// the end.  The arithmetic per element is the graph path's (k_step_x,
+// y_epilogue, t_epilogue, ctrl_*_body).  Vectors written in one phase and read
+// by other CTAs in the next are loaded coherently (ld.global / .cg).
+// ---------------------------------------------------------------------------
+template <int VWY, int VWT>
+__global__ void __launch_bounds__(BS, 1) k_persist(KArgs A, TileSrc SY, TileSrc ST, double* pX, double* pY,
+                                                   double* pT, int cap, long long max_trials) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ PdcsCtrl sc;
+  __shared__ double sred[16];
+  constexpr int NW = sizeof(PdcsCtrl) / sizeof(long long);
+  for (int i = threadIdx.x; i < NW; i += blockDim.x)
+    reinterpret_cast<long long*>(&sc)[i] = reinterpret_cast<const long long*>(A.ctrl)[i];
+  __syncthreads();
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), wt = gridDim.x * (blockDim.x >> 5);
+  long long trials = 0;
+  while (!sc.stop && trials < max_trials) {
+    ++trials;
+    {  // X: pending Halpern + primal candidate (k_step_x)
+      const bool pend = sc.pending != 0;
+      const bool inject = sc.nan_after >= 0 && sc.n_primal_proj >= sc.nan_after;
+      const double a = sc.pa, b = sc.pb, be = sc.pbeta, et = sc.peta, W = sc.pW, tau = sc.tau;
+      const double opb = 1.0 + be, tot = W + et;
+      double acc[GX_N] = {0.0, 0.0, 0.0};
+      for (int j = gtid; j < A.n; j += gstride) {
+        double xn, gn;
+        if (pend) {
+          const double xo = A.x[j];
+          xn = a * (opb * A.xh[j] - be * xo) + b * __ldg(A.xa + j);
+          const double go = A.gty[j];
+          // G^T y_hat was written by other CTAs in the last T phase: L2 load
+          gn = a * (opb * __ldcg(A.gth + j) - be * go) + b * __ldg(A.gtya + j);
+          A.xb[j] = (W == 0.0) ? xn : (W * A.xb[j] + et * xn) / tot;
+          A.x[j] = xn;
+          A.gty[j] = gn;
+        } else {
+          xn = A.x[j];
+          gn = A.gty[j];
+        }
+        const double cj = __ldg(A.c + j);
+        const double v = xn - tau * (cj - gn);
+        double lj, uj;
+        box_bounds<false>(A, j, 0, lj, uj);
+        double p = clampv(v, lj, uj);
+        if (j == 0 && inject) p = __longlong_as_double(0x7ff8000000000000ll);
+        A.xh[j] = p;
+        A.xt[j] = 2.0 * p - xn;
+        const double d = p - xn;
+        acc[GX_XX] += xn * xn;
+        acc[GX_DXDX] += d * d;
+        acc[GX_CX] += cj * p;
+      }
+      block_store_mask<GX_N>(acc, 0u, pX, cap, blockIdx.x);
+    }
+    grid.sync();
+    {  // Y: w = G^ x~ and the dual candidate (k_step_y_lane)
+      const YCoef k = y_coef(&sc);
+      double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      constexpr int RPW = 32 / VWY;
+      const int sub = lane & (VWY - 1);
+      for (int base = wg * RPW; base < A.m; base += wt * RPW) {
+        const int r = base + lane / VWY;
+        const double dot = lane_row<VWY, 3>(SY, A.xt, nullptr, r, sub, A.m, 0, 0);
+        if (sub == 0 && r < A.m) y_epilogue<false>(A, k, r, dot, acc, 0, 0);
+      }
+      block_store_mask<GY_N>(acc, 0u, pY, cap, blockIdx.x);
+    }
+    grid.sync();
+    ctrl_ls_body<1>(&sc, pX, cap, pY, cap, sred, nullptr);
+    __syncthreads();
+    if (sc.stop) break;
+    if (!sc.accepted) {
+      grid.sync();  // the partials are rewritten by the next trial's X
+      continue;
+    }
+    {  // T: G^T y_hat and the beta partials (k_step_t_lane)
+      double acc[GT_N] = {0.0, 0.0, 0.0};
+      constexpr int RPW = 32 / VWT;
+      const int sub = lane & (VWT - 1);
+      for (int base = wg * RPW; base < A.n; base += wt * RPW) {
+        const int j = base + lane / VWT;
+        const double dot = lane_row<VWT, 3>(ST, A.yh, nullptr, j, sub, A.n, 0, 0);
+        if (sub == 0 && j < A.n) t_epilogue<false>(A, j, dot, acc, 0);
+      }
+      block_store_mask<GT_N>(acc, 0u, pT, cap, blockIdx.x);
+    }
+    grid.sync();
+    ctrl_beta_body<1>(&sc, pT, cap, sred, A.err, nullptr);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < NW; i += blockDim.x)
+      reinterpret_cast<long long*>(A.ctrl)[i] = reinterpret_cast<const long long*>(&sc)[i];
   }
 }
 

@@ -299,7 +299,7 @@ def test_solve_many_matches_sequential(P):
     probs = [instances.lp_random(150, 300, 0.05, seed) for seed in range(6)]
     opts = P.SolverOptions(rel_tol=1e-6, abs_tol=1e-6)
     seq = [P.solve(p, opts) for p in probs]
-    par = solve_many(probs, opts, max_workers=6)
+    par = solve_many(probs, opts, max_workers=6, batched=False)
     for a, b in zip(seq, par):
         assert a.exit_status == b.exit_status and a.iterations == b.iterations
         np.testing.assert_array_equal(a.x, b.x)
@@ -455,7 +455,7 @@ def test_solve_many_stress(P):
 
     probs = [instances.lp_random(400, 800, 0.02, seed) for seed in range(24)]
     opts = P.SolverOptions(rel_tol=1e-5, abs_tol=1e-5)
-    par = solve_many(probs, opts, max_workers=12)
+    par = solve_many(probs, opts, max_workers=12, batched=False)
     ref = P.solve(probs[7], opts)
     assert all(r.exit_status == ":optimal" for r in par)
     np.testing.assert_array_equal(par[7].x, ref.x)

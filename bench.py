@@ -511,6 +511,14 @@ def run_ours(args, rank, world, local):
             line["sustained"] = sustained
         if selfcheck:
             line["selfcheck"] = selfcheck
+        ttt_path = os.path.join(REPO, "profiles", "r02_ttt.jsonl")
+        if os.path.exists(ttt_path):
+            # long time-to-tolerance solves (minutes each) recorded by tools/ttt.py in a
+            # separate run on a B200; labelled as recorded, not measured in this run
+            with open(ttt_path) as f:
+                line["recorded_time_to_tolerance"] = {
+                    "source": "profiles/r02_ttt.jsonl (tools/ttt.py, separate run, public solve())",
+                    "runs": [json.loads(x) for x in f if x.strip()]}
         if batched:
             line["batched"] = batched
         emit(line)

@@ -1,5 +1,6 @@
 set -x
 export PYTHONUNBUFFERED=1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2m_smoke.log 2>&1; echo rc=$? >> gpurun_out/r2m_smoke.log
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r2m_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2m_pytest.log
 for t in "" "expminb=2" "expminb=3"; do
   PDCS_TUNE=$t timeout 300 python bench.py --config C3 --steps 2000 --warmup 50 --no-cpu-baseline --no-ttt-c1 --no-e2e >> gpurun_out/r2m_c3.jsonl 2>> gpurun_out/r2m_c3.err

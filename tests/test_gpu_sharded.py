@@ -50,9 +50,17 @@ def test_sharded_world1_matches_single_gpu(group, case):
     # instances), so the contract is status + objective + KKT, and the
     # early trajectory (test below).
     assert rs.exit_status == r1.exit_status == str(d["status"])
-    # the reference's own iteration band under 1-ulp noise, widened by one check
-    # interval (-15%..+4% on C1): |k_sharded - k_single| <= 20% + 2000
-    assert abs(rs.iterations - r1.iterations) <= int(0.2 * r1.iterations) + 2000
+    # inside the reference's own iteration band under 1-ulp
+    # SpMV noise (tests/golden/noise_bands.json) widened by one check interval --
+    # the sharded sums are one more reordering of the same arithmetic
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "noise_bands.json")) as f:
+        _, lo, hi = json.load(f)[case]
+    freq = o.get("duality_gap_restart_freq", 2000)
+    for r in (r1, rs):
+        assert lo - freq <= r.iterations <= hi + freq, (case, r.iterations, lo, hi)
     tol = max(o.get("rel_tol", 1e-6), 1e-6)
     assert abs(rs.p_obj - r1.p_obj) <= tol * (1 + abs(r1.p_obj))
     assert rs.y.shape == r1.y.shape and rs.x.shape == r1.x.shape

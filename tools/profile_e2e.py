@@ -12,7 +12,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(cfg, iters):
+def main(cfg, iters, cold=False):
     import torch
 
     import bench
@@ -23,6 +23,8 @@ def main(cfg, iters):
     opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=iters, time_limit=1e9)
     solve(problem, SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=2, time_limit=1e9))  # warm
     torch.cuda.synchronize()
+    if cold:  # as bench.py's e2e leg: the caching allocator emptied first
+        torch.cuda.empty_cache()
     pr = cProfile.Profile()
     t0 = time.perf_counter()
     pr.enable()
@@ -33,4 +35,5 @@ def main(cfg, iters):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 2000)
+    main(sys.argv[1] if len(sys.argv) > 1 else "C5", int(sys.argv[2]) if len(sys.argv) > 2 else 2000,
+         len(sys.argv) > 3 and sys.argv[3] == "cold")

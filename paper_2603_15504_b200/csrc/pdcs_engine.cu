@@ -764,7 +764,7 @@ int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
   int* cnt = nullptr;
   CK(cudaMallocAsync(&cnt, sizeof(int) * (nflat + 1), s));
   CK(cudaMemsetAsync(cnt, 0, sizeof(int) * (nflat + 1), s));
-  CK(cudaMalloc(&Q.d_po, sizeof(int) * (nflat + 1)));
+  CK(cudaMallocAsync(&Q.d_po, sizeof(int) * (nflat + 1), s));
   k_panel_count<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width, cnt);
   CKL();
   size_t tmp_bytes = 0;
@@ -778,9 +778,10 @@ int build_panels(PanelPlan& Q, const SpmvPlan& P, int np, cudaStream_t s) {
   CK(cudaFreeAsync(cnt, s));
   CK(cudaStreamSynchronize(s));
   Q.nnz_short = total;
-  CK(cudaMalloc(&Q.d_pci, sizeof(int) * std::max(total, 1)));
-  CK(cudaMalloc(&Q.d_pperm, sizeof(int) * std::max(total, 1)));
-  CK(cudaMalloc(&Q.d_pva, sizeof(double) * std::max(total, 1)));
+  // stream-ordered (pooled) allocations: a later engine's setup reuses them
+  CK(cudaMallocAsync(&Q.d_pci, sizeof(int) * std::max(total, 1), s));
+  CK(cudaMallocAsync(&Q.d_pperm, sizeof(int) * std::max(total, 1), s));
+  CK(cudaMallocAsync(&Q.d_pva, sizeof(double) * std::max(total, 1), s));
   k_panel_scatter<<<grid_for(P.nrows), BS, 0, s>>>(P.nrows, P.rowptr, P.colidx, P.long_t, Q.np, Q.width,
                                                    Q.d_po, Q.d_pci, Q.d_pperm);
   CKL();
@@ -795,11 +796,11 @@ int refresh_panel_values(const PanelPlan& Q, const double* val, cudaStream_t s) 
   return 0;
 }
 
-void free_panels(PanelPlan& Q) {
-  cudaFree(Q.d_po);
-  cudaFree(Q.d_pci);
-  cudaFree(Q.d_pva);
-  cudaFree(Q.d_pperm);
+void free_panels(PanelPlan& Q, cudaStream_t s) {
+  if (Q.d_po) cudaFreeAsync(Q.d_po, s);
+  if (Q.d_pci) cudaFreeAsync(Q.d_pci, s);
+  if (Q.d_pva) cudaFreeAsync(Q.d_pva, s);
+  if (Q.d_pperm) cudaFreeAsync(Q.d_pperm, s);
   Q = PanelPlan();
 }
 
@@ -1249,9 +1250,9 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     if ((E->tile_y && !E->soc_tile && build_tiles(E->G, s)) || (E->tile_t && build_tiles(E->GT, s)))
       return fail(1);
     T.lap("tiles");
-    if (E->PG.np > 1 && cudaMalloc(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1)) != cudaSuccess)
+    if (E->PG.np > 1 && cudaMallocAsync(&E->d_wpart_y, sizeof(double) * std::max(d.m, 1), s) != cudaSuccess)
       return fail(1);
-    if (E->PGT.np > 1 && cudaMalloc(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1)) != cudaSuccess)
+    if (E->PGT.np > 1 && cudaMallocAsync(&E->d_wpart_x, sizeof(double) * std::max(d.n, 1), s) != cudaSuccess)
       return fail(1);
     auto fit = [&](const void* fn, int needed) {
       int occ = 0;
@@ -1367,10 +1368,11 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   if (E->graph) cudaGraphDestroy(E->graph);
   free_plan(E->G);
   free_plan(E->GT);
-  free_panels(E->PG);
-  free_panels(E->PGT);
-  cudaFree(E->d_wpart_y);
-  cudaFree(E->d_wpart_x);
+  free_panels(E->PG, E->stream);
+  free_panels(E->PGT, E->stream);
+  if (E->d_wpart_y) cudaFreeAsync(E->d_wpart_y, E->stream);
+  if (E->d_wpart_x) cudaFreeAsync(E->d_wpart_x, E->stream);
+  if (E->stream) cudaStreamSynchronize(E->stream);  // the stream may go away with the caller
   if (E->comm && g_nccl.ok) g_nccl.commDestroy((ncclComm_t)E->comm);
   cudaFree(E->d_yred);
   cudaFree(E->d_gtp);

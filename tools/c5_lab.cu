@@ -170,6 +170,99 @@ __global__ void __launch_bounds__(BS) k_pass(const int* po, const int* ci, const
   }
 }
 
+// ---- TMA-staged pass: each CTA streams a tile of TR rows' offsets, column
+// indices and values into shared memory with cp.async.bulk (no LSU / L1 tag
+// work for the streams), double-buffered; the threads read them with LDS and
+// gather x with LDG (thread per row, index-order sums, as k_pass).
+constexpr int TR = 256;
+constexpr int TE = TR * K + 16;
+struct __align__(16) Stage {
+  int po[TR + 8];
+  int ci[TE];
+  double va[TE];
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+
+template <bool FIRST>
+__global__ void __launch_bounds__(TR, 4) k_pass_tma(const int* po, const int* ci, const double* va,
+                                                    const double* x, const double* win, double* wout) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  Stage* st = reinterpret_cast<Stage*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ int meta[2][3];  // po base row, ci base entry, va base entry
+  const int tid = threadIdx.x;
+  const int ntiles = (M + TR - 1) / TR;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&bar[0])));
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int s, int t) {
+    const int r0 = t * TR, r1 = min(M, r0 + TR);
+    const int e0 = po[r0], e1 = po[r1];
+    const int a0 = r0 & ~3, npo = ((r1 + 1 - a0) + 3) & ~3;
+    const int c0 = e0 & ~3, nci = ((e1 - c0) + 3) & ~3;
+    const int v0 = e0 & ~1, nva = ((e1 - v0) + 1) & ~1;
+    meta[s][0] = a0; meta[s][1] = c0; meta[s][2] = v0;
+    const uint32_t bytes = npo * 4 + nci * 4 + nva * 8;
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(&bar[s])), "r"(bytes));
+    bulk(st[s].po, po + a0, npo * 4, &bar[s]);
+    if (nci) bulk(st[s].ci, ci + c0, nci * 4, &bar[s]);
+    if (nva) bulk(st[s].va, va + v0, nva * 8, &bar[s]);
+  };
+  int t = blockIdx.x;
+  if (tid == 0) {
+    if (t < ntiles) issue(0, t);
+    if (t + (int)gridDim.x < ntiles) issue(1, t + gridDim.x);
+  }
+  uint32_t phase[2] = {0, 0};
+  for (int k = 0; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k & 1;
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(su32(&bar[s])), "r"(phase[s]) : "memory");
+    phase[s] ^= 1;
+    const int r0 = t * TR, r = r0 + tid;
+    const int a0 = meta[s][0], c0 = meta[s][1], v0 = meta[s][2];
+    if (r < M) {
+      const int b = st[s].po[r - a0], e = st[s].po[r + 1 - a0];
+      double acc = FIRST ? 0.0 : win[r];
+      for (int j = b; j < e; j += 4) {
+        const int q = e - j;
+        const int cc0 = st[s].ci[j - c0];
+        const int cc1 = q > 1 ? st[s].ci[j + 1 - c0] : 0, cc2 = q > 2 ? st[s].ci[j + 2 - c0] : 0,
+                  cc3 = q > 3 ? st[s].ci[j + 3 - c0] : 0;
+        const double w0 = st[s].va[j - v0];
+        const double w1 = q > 1 ? st[s].va[j + 1 - v0] : 0.0, w2 = q > 2 ? st[s].va[j + 2 - v0] : 0.0,
+                     w3 = q > 3 ? st[s].va[j + 3 - v0] : 0.0;
+        const double x0 = __ldg(x + cc0);
+        const double x1 = q > 1 ? __ldg(x + cc1) : 0.0, x2 = q > 2 ? __ldg(x + cc2) : 0.0,
+                     x3 = q > 3 ? __ldg(x + cc3) : 0.0;
+        acc += w0 * x0;
+        if (q > 1) acc += w1 * x1;
+        if (q > 2) acc += w2 * x2;
+        if (q > 3) acc += w3 * x3;
+      }
+      wout[r] = acc;
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0 && t + 2 * (int)gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(s, t + 2 * gridDim.x);
+    }
+  }
+}
+
 __device__ __forceinline__ void yepi(const Y& Yv, int r, double dot, double* acc) {
   const double yo = Yv.y[r];
   const double yn = 0.9 * Yv.yh[r] + 0.05 * yo + 0.05 * Yv.ya[r];
@@ -242,7 +335,7 @@ Panels build(const int* d_col, const double* d_val, std::vector<int> cuts) {
   int* cnt;
   CK(cudaMalloc(&cnt, sizeof(int) * ((size_t)Q.P * M + 1)));
   k_count<<<4096, BS>>>(d_col, d_cuts, Q.P, cnt);
-  CK(cudaMalloc(&Q.d_po, sizeof(int) * ((size_t)Q.P * M + 1)));
+  CK(cudaMalloc(&Q.d_po, sizeof(int) * ((size_t)Q.P * M + 1 + 64)));
   void* tmp = nullptr;
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, Q.d_po, (int)((size_t)Q.P * M + 1));
@@ -250,8 +343,8 @@ Panels build(const int* d_col, const double* d_val, std::vector<int> cuts) {
   CK(cudaMemset(cnt + (size_t)Q.P * M, 0, sizeof(int)));
   cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, Q.d_po, (int)((size_t)Q.P * M + 1));
   CK(cudaDeviceSynchronize());
-  CK(cudaMalloc(&Q.d_pci, sizeof(int) * (size_t)M * K));
-  CK(cudaMalloc(&Q.d_pva, sizeof(double) * (size_t)M * K));
+  CK(cudaMalloc(&Q.d_pci, sizeof(int) * ((size_t)M * K + 64)));
+  CK(cudaMalloc(&Q.d_pva, sizeof(double) * ((size_t)M * K + 64)));
   k_scatter<<<4096, BS>>>(d_col, d_val, d_cuts, Q.P, Q.d_po, Q.d_pci, Q.d_pva);
   CK(cudaDeviceSynchronize());
   cudaFree(tmp);
@@ -297,6 +390,13 @@ int main(int argc, char** argv) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, k_xstep, BS, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_epi, k_epi, BS, 0);
   const int gp = occ_pass * nsm, gf = occ_fin * nsm, gx = occ_x * nsm, ge = occ_epi * nsm;
+  const size_t tma_smem = 2 * sizeof(Stage) + 128;
+  CK(cudaFuncSetAttribute(k_pass_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
+  CK(cudaFuncSetAttribute(k_pass_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
+  int occ_tma = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tma, k_pass_tma<false>, TR, tma_smem);
+  const int gtma = occ_tma * nsm;
+  printf("tma pass: %zu B smem per CTA, %d CTAs/SM\n", tma_smem, occ_tma);
   printf("grids pass %d final %d xstep %d epi %d\n", gp, gf, gx, ge);
 
   cudaEvent_t e0, e1, e2, e3;
@@ -305,16 +405,15 @@ int main(int argc, char** argv) {
     k_xstep<<<gx, BS>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6], xs[7], xs[8], xs[9], xs[10], xt, part);
   };
 
-  struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; int gmode = 0; };
+  struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; int gmode = 0; int tma = 0; };
   // fr: panel width fractions; order 0 = panels 0..P-1, 1 = reversed; split: epilogue in its own kernel
   std::vector<Variant> V = {
       {"P3 equal fwd (current)", {1, 1, 1}, 0, 0},
       {"P3 split-epi evict_first", {1, 1, 1}, 0, 1, 1},
-      {"P3 split-epi NO GATHER", {1, 1, 1}, 0, 1, 0, 1},
-      {"P1 split-epi NO GATHER", {1}, 0, 1, 0, 1},
-      {"P1 split-epi gather", {1}, 0, 1, 0, 0},
-      {"P2 split-epi evict_first", {1, 1}, 0, 1, 1},
-      {"P4 split-epi evict_first", {1, 1, 1, 1}, 0, 1, 1},
+      {"P3 split-epi TMA-staged passes", {1, 1, 1}, 0, 1, 0, 0, 1},
+      {"P3 split-epi plain passes", {1, 1, 1}, 0, 1, 0, 0, 0},
+      {"P4 split-epi TMA-staged passes", {1, 1, 1, 1}, 0, 1, 0, 0, 1},
+      {"P2 split-epi TMA-staged passes", {1, 1}, 0, 1, 0, 0, 1},
   };
   for (const Variant& v : V) {
     double tot = 0;
@@ -339,7 +438,11 @@ int main(int argc, char** argv) {
         const int p = ord[i];
         const int* po = Q.d_po + (size_t)p * M;
         double* wo = bufs[i & 1];
-        if (v.gmode == 1) {
+        if (v.tma) {
+          const size_t smem = 2 * sizeof(Stage) + 128;
+          if (i == 0) k_pass_tma<true><<<gtma, TR, smem>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+          else k_pass_tma<false><<<gtma, TR, smem>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+        } else if (v.gmode == 1) {
           if (i == 0) k_pass<true, 0, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
           else k_pass<false, 0, 1><<<gp, BS>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
         } else if (v.mode == 1) {
@@ -372,8 +475,15 @@ int main(int argc, char** argv) {
       if (it >= 2) { best = std::min(best, ms); sum += ms; xbest = std::min(xbest, xms); ebest = std::min(ebest, ems); }
     }
     CK(cudaGetLastError());
-    printf("%-28s ystep best %.4f ms avg %.4f ms   (xstep %.4f ms, epilogue %.4f ms)\n", v.name, best,
-           sum / reps, xbest, v.split ? ebest : 0.0f);
+    double cs = 0.0;
+    if (v.split) {  // checksum of the product w the passes produced (bit-identical schedules agree)
+      std::vector<double> hw(M);
+      const int npass = P;
+      CK(cudaMemcpy(hw.data(), (npass - 1) & 1 ? wB : wA, sizeof(double) * M, cudaMemcpyDeviceToHost));
+      for (double vv : hw) cs += vv;
+    }
+    printf("%-34s ystep best %.4f ms avg %.4f ms   (xstep %.4f ms, epilogue %.4f ms) w-sum %.17g\n", v.name,
+           best, sum / reps, xbest, v.split ? ebest : 0.0f, cs);
     fflush(stdout);
     free_panels(Q);
   }

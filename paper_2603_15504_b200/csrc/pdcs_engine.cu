@@ -1319,7 +1319,12 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     if (!off && coop && vw_ok && !E->has_xblocks && !E->has_yblocks && E->G.n_long == 0 &&
         E->GT.n_long == 0 && E->PG.np == 1 && E->PGT.np == 1 && !E->tile_y && !E->tile_t && !E->split &&
         d.nnz <= (1 << 22) && d.n > 0 && d.m > 0) {
-      E->pgrid = nsm;
+      // one CTA per SM: measured best for one C1 solve (55.3k it/s against 51.4k at 74
+      // CTAs, 38.7k at 37, 27.9k at 18; profiles/r02_sweeps.txt).  Concurrent small
+      // solves belong in batch.solve_many (one graph for all), not in host threads
+      // each launching a whole-GPU cooperative kernel.  PDCS_TUNE pgrid=N overrides.
+      const char* pg = env ? strstr(env, "pgrid=") : nullptr;
+      E->pgrid = pg ? std::max(1, std::min(nsm, atoi(pg + 6))) : nsm;
       if (cudaMalloc(&E->d_pX, sizeof(double) * GX_N * E->pgrid) == cudaSuccess &&
           cudaMalloc(&E->d_pY, sizeof(double) * GY_N * E->pgrid) == cudaSuccess &&
           cudaMalloc(&E->d_pT, sizeof(double) * GT_N * E->pgrid) == cudaSuccess)

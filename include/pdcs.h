@@ -320,6 +320,11 @@ int pdcs_unscale(PdcsEngine* e, const double* d_x, const double* d_y, const doub
  * arrays); an optimisation of the same arithmetic. */
 int pdcs_engine_set_uniform_box(PdcsEngine* e, double lo, double hi);
 
+/* Small block-free engines run their trials in one cooperative launch per
+ * pdcs_run_inner (chosen at create); on = 0 keeps them on the CUDA-graph path
+ * (solves on concurrent host threads: a cooperative launch occupies the GPU). */
+int pdcs_engine_set_persist(PdcsEngine* e, int32_t on);
+
 /* ---- multi-GPU ------------------------------------------------
  * A sharded solve gives every rank a contiguous row slice of G^ (cut at dual
  * cone-block boundaries) and a contiguous x-slice (cut at primal cone-block

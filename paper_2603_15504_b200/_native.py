@@ -120,6 +120,7 @@ _SIGS = {
     "pdcs_debug_inject_nan": (C.c_int, [_P, C.c_int64]),
     "pdcs_comm_unique_id": (C.c_int, [C.c_char_p]),
     "pdcs_engine_set_uniform_box": (C.c_int, [_P, C.c_double, C.c_double]),
+    "pdcs_engine_set_persist": (C.c_int, [_P, C.c_int32]),
     "pdcs_engine_set_comm": (C.c_int, [_P, C.c_char_p, C.c_int32, C.c_int32]),
     "pdcs_engine_set_xsplit": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_int32]),
     "pdcs_allgather_x": (C.c_int, [_P, C.POINTER(C.c_void_p), C.c_int32]),

@@ -16,8 +16,10 @@ reference solves one problem per call (engine.py:683-689); here
 * ``batched=False`` is the plain thread pool: one engine, one stream and its
   own graph replays per instance.
 
-Either way every solve is the deterministic single-instance solve: results
-are bit-identical to calling `solve` one by one.
+Either way every member runs the graph-path kernels of a single solve, so
+results are bit-identical to `solve` calls on the graph path (`PDCS_TUNE=
+persist=0`); a lone small solve runs the persistent kernel instead, whose
+reductions are grouped differently (equal to rounding).
 """
 
 from __future__ import annotations
@@ -108,9 +110,17 @@ def solve_many(problems, options: SolverOptions | None = None, max_workers: int 
         raise ValueError("solve_many does not support iteration callbacks")
     options.validate()
     if not batched:
+        from .device import _thread_opts
+
+        def one(p):
+            # concurrent solves stay on the graph path (a persistent cooperative
+            # launch of a small solve would occupy the whole GPU)
+            _thread_opts.no_persist = True
+            return solve(p, options)
+
         workers = max_workers or min(16, len(problems))
         with ThreadPoolExecutor(max_workers=workers) as pool:
-            return list(pool.map(lambda p: solve(p, options), problems))
+            return list(pool.map(one, problems))
 
     probs = [p if isinstance(p, ConicProblem) else _adopt(p) for p in problems]
     # engines (upload, transpose, panels, preconditioning) on a pool of threads

@@ -2093,6 +2093,12 @@ int pdcs_comm_unique_id(unsigned char* h_id) {
   return 0;
 }
 
+int pdcs_engine_set_persist(PdcsEngine* E, int32_t on) {
+  if (!E) { g_err = "pdcs_engine_set_persist: null engine"; return 2; }
+  E->persist = on && E->d_pX != nullptr;  // only engines set up for it at create
+  return 0;
+}
+
 int pdcs_engine_set_uniform_box(PdcsEngine* E, double lo, double hi) {
   if (!E) { g_err = "pdcs_engine_set_uniform_box: null engine"; return 2; }
   const char* env = getenv("PDCS_TUNE");

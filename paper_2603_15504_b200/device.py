@@ -63,6 +63,9 @@ def _slab(dtype, sizes: dict, align: int = 64) -> dict:
 
 _STAGE_BYTES = 32 << 20
 _stage_local = threading.local()
+# set by batch.solve_many's thread-pool path: engines built on this thread stay
+# on the CUDA-graph path (a persistent cooperative launch occupies the GPU)
+_thread_opts = threading.local()
 _COPY_THREADS = 4
 _copy_pool = None
 _copy_lock = threading.Lock()
@@ -330,6 +333,8 @@ class DeviceEngine:
                 "pdcs_engine_create")
         self.handle = h
         self.asis = asis
+        if getattr(_thread_opts, "no_persist", False):
+            N.check(lib.pdcs_engine_set_persist(h, 0), "pdcs_engine_set_persist")
         nb = work.num_box
         if nb > 0:
             l0, u0 = np.asarray(work.l[:nb]), np.asarray(work.u[:nb])

@@ -71,7 +71,7 @@ def test_batched_many_c1_class_and_large_uploads(monkeypatch):
         _same(_graph_solve(P, probs[i], opts, monkeypatch), bat[i])
 
 
-def test_threaded_solve_many_large_instances():
+def test_threaded_solve_many_large_instances(monkeypatch):
     """The thread-pool path with instances above the staging threshold."""
     import paper_2603_15504_b200 as P
     from paper_2603_15504_b200 import instances
@@ -81,7 +81,7 @@ def test_threaded_solve_many_large_instances():
     opts = P.SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=300)
     par = solve_many(probs, opts, batched=False, max_workers=6)
     for i in (0, 5):
-        _same(P.solve(probs[i], opts), par[i])
+        _same(_graph_solve(P, probs[i], opts, monkeypatch), par[i])
 
 
 def test_persistent_path_matches_graph_path_to_rounding(monkeypatch):

@@ -290,7 +290,7 @@ def test_full_size_c5_spmv_is_bit_identical_to_scipy(P):
     assert abs(float(y @ gx) - float(gty @ x)) <= 1e-9 * abs(float(y @ gx))
 
 
-def test_solve_many_matches_sequential(P):
+def test_solve_many_matches_sequential(P, monkeypatch):
     """Concurrent solves (one engine + stream per instance, host threads) give
     the bit-identical results of sequential solves."""
     from paper_2603_15504_b200 import instances
@@ -298,7 +298,9 @@ def test_solve_many_matches_sequential(P):
 
     probs = [instances.lp_random(150, 300, 0.05, seed) for seed in range(6)]
     opts = P.SolverOptions(rel_tol=1e-6, abs_tol=1e-6)
+    monkeypatch.setenv("PDCS_TUNE", "persist=0")  # the thread pool keeps the graph path
     seq = [P.solve(p, opts) for p in probs]
+    monkeypatch.delenv("PDCS_TUNE")
     par = solve_many(probs, opts, max_workers=6, batched=False)
     for a, b in zip(seq, par):
         assert a.exit_status == b.exit_status and a.iterations == b.iterations
@@ -447,7 +449,7 @@ def test_giant_soc_plain_projection_matches_oracle(P):
         np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * (1 + np.abs(want).max()))
 
 
-def test_solve_many_stress(P):
+def test_solve_many_stress(P, monkeypatch):
     """Many concurrent solves: setup, graph capture and check paths of one
     engine overlap other threads' work (no device-wide syncs allowed)."""
     from paper_2603_15504_b200 import instances
@@ -456,6 +458,7 @@ def test_solve_many_stress(P):
     probs = [instances.lp_random(400, 800, 0.02, seed) for seed in range(24)]
     opts = P.SolverOptions(rel_tol=1e-5, abs_tol=1e-5)
     par = solve_many(probs, opts, max_workers=12, batched=False)
+    monkeypatch.setenv("PDCS_TUNE", "persist=0")
     ref = P.solve(probs[7], opts)
     assert all(r.exit_status == ":optimal" for r in par)
     np.testing.assert_array_equal(par[7].x, ref.x)

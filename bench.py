@@ -405,9 +405,10 @@ def run_ours(args, rank, world, local):
     peak, peak_kind = peaks()
     b_alg = instances.algorithmic_bytes(problem)
     iter_gbs = b_alg * (iters / (ms / 1000.0)) / 1e9
-    dom = max(stages, key=lambda s: s[1]) if stages else ("step_y_spmv", float("nan"))
+    dom = max(stages, key=lambda s: s[1]) if stages else ("step_y_spmv", None)
     dom_bytes = kernel_bytes(problem, dom[0])
-    dom_gbs = dom_bytes / (dom[1] / 1000.0) / 1e9 if dom[1] > 0 else float("nan")
+    # no per-stage profile (--profile-reps 0): no kernel roofline (null, not NaN)
+    dom_gbs = dom_bytes / (dom[1] / 1000.0) / 1e9 if dom[1] else None
     slot_ms = sum(s[1] for s in stages)
     del loop
     torch.cuda.empty_cache()
@@ -495,7 +496,7 @@ def run_ours(args, rank, world, local):
                     "instance_gen_s": gen_s, "launch": launch_info, "tune": os.environ.get("PDCS_TUNE", ""),
                     "host": host_info()},
             "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": dom_gbs, "peak": peak,
-                         "unit": "GB/s", "frac": dom_gbs / peak,
+                         "unit": "GB/s", "frac": dom_gbs / peak if dom_gbs is not None else None,
                          "traffic": measured_traffic(args.config, dom[0]),
                          "bytes_per_launch": dom_bytes, "launch_ms": dom[1], "peak_source": peak_kind},
             "iteration_roofline": {"B_alg_bytes": b_alg, "achieved": iter_gbs, "peak": peak, "unit": "GB/s",

@@ -326,7 +326,63 @@ int build_tiles(SpmvPlan& P, cudaStream_t s, const std::vector<int>* head = null
   return 0;
 }
 
+// PDCS_TUNE="key=value,..." launch-configuration override (dflt when absent)
+double tune_env(const char* key, double dflt) {
+  const char* env = getenv("PDCS_TUNE");
+  if (!env) return dflt;
+  std::string s(env), k = std::string(key) + "=";
+  size_t p = s.find(k);
+  if (p == std::string::npos || (p > 0 && s[p - 1] != ',')) return dflt;
+  return atof(s.c_str() + p + k.size());
+}
+
+// Row classes for the class-split step SpMV (mixed row lengths, no chunked
+// long rows): the rows of more than CLS_SHORT entries, listed ascending (the
+// epilogue sums the short ones), and the lanes per long row.
+struct IsLongClassRow {
+  const int* rp;
+  __host__ __device__ bool operator()(int r) const { return rp[r + 1] - rp[r] > CLS_SHORT; }
+};
+
+int build_classes(SpmvPlan& P, cudaStream_t s, int nsm) {
+  const int nrows = P.nrows;
+  unsigned long long* st = nullptr;
+  CK(cudaMallocAsync(&st, sizeof(unsigned long long) * 4, s));
+  CK(cudaMemsetAsync(st, 0, sizeof(unsigned long long) * 4, s));
+  k_row_stats<<<grid_for(nrows), BS, 0, s>>>(P.rowptr, nrows, CLS_SHORT, st);
+  CKL();
+  unsigned long long h[4];
+  CK(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaFreeAsync(st, s));
+  P.n_cls_short = (int)h[2];
+  P.n_cls_long = (int)h[3];
+  const double mean_long = P.n_cls_long ? (double)(P.nnz - (long long)h[0]) / P.n_cls_long : 0.0;
+  // lanes per long row: about 4-8 entries per lane (PDCS_TUNE cls_vw=8|16|32)
+  const int vw = (int)tune_env("cls_vw", mean_long <= 64.0 ? 8.0 : (mean_long <= 160.0 ? 16.0 : 32.0));
+  P.cls_vw = vw == 32 ? 32 : (vw == 16 ? 16 : 8);
+  CK(cudaMalloc(&P.d_cls_long, sizeof(int) * std::max(P.n_cls_long, 1)));
+  int* num = nullptr;
+  CK(cudaMallocAsync(&num, sizeof(int), s));
+  thrust::counting_iterator<int> it(0);
+  size_t tb = 0;
+  CK(cub::DeviceSelect::If(nullptr, tb, it, P.d_cls_long, num, nrows, IsLongClassRow{P.rowptr}, s));
+  void* tmp = nullptr;
+  CK(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), s));
+  CK(cub::DeviceSelect::If(tmp, tb, it, P.d_cls_long, num, nrows, IsLongClassRow{P.rowptr}, s));
+  CK(cudaFreeAsync(tmp, s));
+  CK(cudaFreeAsync(num, s));
+  CK(cudaStreamSynchronize(s));
+  int occ = 1;
+  const void* fn = P.cls_vw == 32 ? (const void*)k_rows_pass<32>
+                                  : (P.cls_vw == 16 ? (const void*)k_rows_pass<16> : (const void*)k_rows_pass<8>);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BS, 0) != cudaSuccess || occ < 1) occ = 1;
+  P.cls_grid_l = std::max(1, std::min(grid_for(P.n_cls_long, BS / P.cls_vw, 1 << 30), occ * nsm));
+  return 0;
+}
+
 void free_plan(SpmvPlan& P) {
+  cudaFree(P.d_cls_long);
   cudaFree(P.d_long_rows);
   cudaFree(P.d_long_first);
   cudaFree(P.d_chunks);
@@ -613,7 +669,7 @@ int split_y(Engine* E, const KArgs& A) {
   if (E->vec && E->m_elem == E->m)
     CK(launch_step(use_pdl(E), k_y_epi2, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
   else
-    CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E)));
+    CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E), ShortRows{}));
   CKL();
   return 0;
 }
@@ -622,9 +678,9 @@ template <bool HS>
 int split_t(Engine* E, const KArgs& A) {
   if (split_passes<1, 0, HS>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->d.d_gth, 2, E->keep_yh)) return 1;
   if (E->vec && E->ubox && E->nbox == E->n)
-    CK(launch_step(use_pdl(E), k_t_epi2, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
+    CK(launch_step(use_pdl(E), k_t_epi2, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E), ShortRows{}));
   else
-    CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E)));
+    CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E), ShortRows{}));
   CKL();
   return 0;
 }
@@ -677,7 +733,39 @@ int launch_gt_partial(Engine* E) {
   }
 }
 
+// class-split step: short rows thread per row, long rows cls_vw lanes per row,
+// the product into `out`, then the streaming epilogue
+int class_pass(Engine* E, const SpmvPlan& P, const double* x, double* out, int gate) {
+  if (!P.n_cls_long) return 0;
+  const PdcsCtrl* c = E->d_ctrl;
+  auto fn = P.cls_vw == 32 ? k_rows_pass<32> : P.cls_vw == 16 ? k_rows_pass<16> : k_rows_pass<8>;
+  CK(launch_step(use_pdl(E), fn, P.cls_grid_l, E->stream, (const int*)P.d_cls_long, P.n_cls_long,
+                 P.rowptr, P.colidx, (const double*)P.val, x, out, c, gate));
+  CKL();
+  return 0;
+}
+
+int class_y(Engine* E, const KArgs& A) {
+  if (class_pass(E, E->G, E->d.d_xt, E->d.d_w, 1)) return 1;
+  const ShortRows R{E->G.rowptr, E->G.colidx, E->G.val, E->d.d_xt};
+  CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E), R));
+  CKL();
+  return 0;
+}
+
+int class_t(Engine* E, const KArgs& A) {
+  if (class_pass(E, E->GT, E->d.d_yh, E->d.d_gth, 2)) return 1;
+  const ShortRows R{E->GT.rowptr, E->GT.colidx, E->GT.val, E->d.d_yh};
+  if (E->vec && E->ubox && E->nbox == E->n)
+    CK(launch_step(use_pdl(E), k_t_epi2, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E), R));
+  else
+    CK(launch_step(use_pdl(E), k_t_epi<false>, E->GT.grid, E->stream, A, E->d_partT, E->capT, fuse_beta(E), R));
+  CKL();
+  return 0;
+}
+
 int launch_step_y(Engine* E, const KArgs& A) {
+  if (E->cls_y) return class_y(E, A);
   if (E->split) return E->hs ? split_y<true>(E, A) : split_y<false>(E, A);
   if (E->tile_y) {
     if (launch_panel_passes(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, E->G.grid, 1)) return 1;
@@ -700,6 +788,7 @@ int launch_step_y(Engine* E, const KArgs& A) {
 }
 
 int launch_step_t(Engine* E, const KArgs& A) {
+  if (E->cls_t) return class_t(E, A);
   if (E->split) return E->hs ? split_t<true>(E, A) : split_t<false>(E, A);
   if (E->tile_t) {
     if (launch_panel_passes(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, E->GT.grid, 2)) return 1;
@@ -1165,14 +1254,7 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     // PDCS_TUNE="py=3,pt=2,panel_mb=48,gx=8,gy=5,gt=6" overrides (panels of the
     // G^ / G^T step SpMVs, gathered-slice budget, CTAs per SM of step kernels)
-    auto tune = [](const char* key, double dflt) {
-      const char* env = getenv("PDCS_TUNE");
-      if (!env) return dflt;
-      std::string s(env), k = std::string(key) + "=";
-      size_t p = s.find(k);
-      if (p == std::string::npos || (p > 0 && s[p - 1] != ',')) return dflt;
-      return atof(s.c_str() + p + k.size());
-    };
+    auto tune = [](const char* key, double dflt) { return tune_env(key, dflt); };
     // Column panels: cut the gathered vector into slices of at most ~0.42 L2.
     // Random 8-byte gathers stay L2-rate bound only while their footprint is
     // below ~50 MB on B200 (tools/gather_probe.cu: 267 G/s up to 48 MB, 196 at
@@ -1287,6 +1369,29 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       E->G.grid = grid_per_sm("gy", ny, fit(ye, ny));
       E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
                                                 : fit((const void*)k_t_epi<false>, nx));
+    }
+    // class split (mixed row lengths, one panel, no chunked long rows; PDCS_TUNE
+    // cls=0 off): rows of > 6 entries 8/16/32 lanes per row, then the streaming
+    // epilogue, which sums the short rows itself; replaces the tiled / 8-lane step of C2-class matrices
+    {
+      const bool cls_on = tune("cls", 1.0) > 0.0;
+      const double cls_nnz = tune("cls_nnz", (double)(1 << 20));
+      auto mixed = [&](const SpmvPlan& P, const PanelPlan& Q) {
+        return cls_on && !E->split && P.n_long == 0 && Q.np == 1 && P.len_cv > 0.5 && (double)d.nnz >= cls_nnz;
+      };
+      if (mixed(E->G, E->PG)) {
+        if (build_classes(E->G, s, nsm)) return fail(1);
+        E->cls_y = true;
+        const int ny = grid_for(d.m, BS, 1 << 30);
+        E->G.grid = grid_per_sm("gy", ny, fit((const void*)k_y_epi<false>, ny));
+      }
+      if (mixed(E->GT, E->PGT)) {
+        if (build_classes(E->GT, s, nsm)) return fail(1);
+        E->cls_t = true;
+        const int nx = grid_for(d.n, BS, 1 << 30);
+        E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
+                                                  : fit((const void*)k_t_epi<false>, nx));
+      }
     }
     // the partial-sum passes are latency bound (dependent rowptr -> col ->
     // gather chains): they get every warp slot their registers allow

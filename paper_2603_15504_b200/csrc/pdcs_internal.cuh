@@ -29,6 +29,11 @@ struct SpmvPlan {
   int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
   double* d_chunk_out = nullptr;  // [n_chunks]
   int grid = 1;                   // CTAs of the short-row kernel
+  // row classes of a mixed-length matrix (class split): the rows of more than
+  // CLS_SHORT entries (cls_vw lanes per row); the epilogue sums the others
+  int* d_cls_long = nullptr;
+  int n_cls_short = 0, n_cls_long = 0, cls_vw = 8;
+  int cls_grid_l = 1;
   int pass_grid = 1;              // CTAs of the panel partial-sum passes (k_lane_pass)
   int* d_tiles = nullptr;         // [ntiles + 1] CSR-stream tile boundaries (rows)
   int ntiles = 0;
@@ -128,6 +133,7 @@ struct Engine {
   bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
   bool soc_tile = false;  // dual SOC blocks projected inside the tiled y-step (d_rowhead)
   bool vec = false;       // 16-byte streaming epilogues of the split step
+  bool cls_y = false, cls_t = false;  // class-split step SpMVs (mixed row lengths)
   bool persist = false;   // small instances: one cooperative launch runs all trials (k_persist)
   int pgrid = 0;          // its grid (one CTA per SM)
   double *d_pX = nullptr, *d_pY = nullptr, *d_pT = nullptr;  // its partial slots [NQ][pgrid]

@@ -1363,6 +1363,27 @@ __global__ void __launch_bounds__(BS) k_lane_pass(TileSrc S, int nrows, const do
   }
 }
 
+// Class split (mixed row lengths): rows of <= CLS_SHORT entries are summed by
+// the epilogue thread itself, in index order, and the product stored back
+// (w / gth stay complete for the block kernels after the epilogue); the rows
+// of the long class come from the k_rows_pass before it.
+constexpr int CLS_SHORT = 6;
+struct ShortRows {
+  const int* rp;  // nullptr: every product comes from the pass (no class split)
+  const int* ci;
+  const double* va;
+  const double* x;
+};
+__device__ __forceinline__ double cls_dot(const ShortRows& R, int r, double w, double* out) {
+  if (R.rp == nullptr) return w;
+  const int b = __ldg(R.rp + r), e = __ldg(R.rp + r + 1);
+  if (e - b > CLS_SHORT) return w;
+  double s = 0.0;
+  for (int j = b; j < e; ++j) s += __ldg(R.va + j) * R.x[__ldg(R.ci + j)];
+  out[r] = s;
+  return s;
+}
+
 // ---- 16-byte (double2) streaming variants of the step epilogues -------------
 // The same per-element arithmetic as k_step_x / y_epilogue / t_epilogue, with
 // every stream moved as aligned pairs (one 16-byte load or store per two
@@ -1569,7 +1590,7 @@ __device__ __forceinline__ void t_elem(const KArgs& A, double dot, double cj, do
 }
 
 // needs a uniform box over all of x-space (ub != 0, nbox == n)
-__global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap, CtrlFuse F) {
+__global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap, CtrlFuse F, ShortRows R) {
   pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
@@ -1579,15 +1600,74 @@ __global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap
   for (int q = tid; q < np; q += nt) {
     const double2 g = ldc2(A.gth, q), c = ld2(A.c, q);
     const double2 d = A.ub == 1 ? ld2(A.d2, q) : make_double2(1.0, 1.0);
-    t_elem(A, g.x, c.x, d.x, acc);
-    t_elem(A, g.y, c.y, d.y, acc);
+    t_elem(A, cls_dot(R, 2 * q, g.x, A.gth), c.x, d.x, acc);
+    t_elem(A, cls_dot(R, 2 * q + 1, g.y, A.gth), c.y, d.y, acc);
   }
   if ((A.nbox & 1) && tid == 0) {
     const int j = A.nbox - 1;
-    t_elem(A, A.gth[j], A.c[j], A.ub == 1 ? A.d2[j] : 1.0, acc);
+    t_elem(A, cls_dot(R, j, A.gth[j], A.gth), A.c[j], A.ub == 1 ? A.d2[j] : 1.0, acc);
   }
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
   fused_ctrl(F);
+}
+
+// Row-class pass of a mixed-length matrix (C2: rows of 1-2 and of ~48
+// entries): the rows of the long class, listed in `rows`, VW lanes per row,
+// product into out[row].  The epilogue then streams over all rows and sums
+// the short ones itself (cls_dot).
+template <int VW>
+__global__ void __launch_bounds__(BS) k_rows_pass(const int* __restrict__ rows, int nr, const int* __restrict__ rp,
+                                                  const int* __restrict__ ci, const double* __restrict__ va,
+                                                  const double* __restrict__ x, double* out, const PdcsCtrl* ctrl,
+                                                  int gate) {
+  pdl_enter();
+  if (gated(ctrl, gate)) return;
+  const int lane = threadIdx.x & 31, sub = lane & (VW - 1);
+  constexpr int RPW = 32 / VW, U = 4;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wt = gridDim.x * (blockDim.x >> 5);
+  // the next row's extent is loaded while this row's entries are summed: the
+  // rows -> rp -> (ci, va) -> x chain is latency bound, not bandwidth bound
+  int i = wg * RPW + lane / VW;
+  int r = 0, b = 0, e = 0;
+  if (i < nr) {
+    r = __ldg(rows + i);
+    b = __ldg(rp + r);
+    e = __ldg(rp + r + 1);
+  }
+  for (int base = wg * RPW; base < nr; base += wt * RPW) {
+    const int in = i + wt * RPW;
+    int rn = 0, bn = 0, en = 0;
+    if (in < nr) {
+      rn = __ldg(rows + in);
+      bn = __ldg(rp + rn);
+      en = __ldg(rp + rn + 1);
+    }
+    double s = 0.0;
+    // U entries per lane in flight: their column and value loads, then the gathers
+    for (int j = b + sub; j < e; j += U * VW) {
+      int c[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int jj = j + u * VW;
+        c[u] = jj < e ? __ldg(ci + jj) : -1;
+        v[u] = jj < e ? __ldg(va + jj) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s += v[u] * __ldg(x + c[u]);
+    }
+    if (VW > 1) {
+#pragma unroll
+      for (int off = VW / 2; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off, VW);
+    }
+    if (sub == 0 && i < nr) out[r] = s;
+    i = in;
+    r = rn;
+    b = bn;
+    e = en;
+  }
 }
 
 // Split step (PDCS_TUNE split=1, matrices without chunked long rows): every
@@ -1596,7 +1676,7 @@ __global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap
 // the y- (x-) space -- the gathered panel no longer competes in L2 with the
 // 13 epilogue streams (C5 lab: 0.486 vs 0.517 ms per y-step with hs=1).
 template <bool H>
-__global__ void __launch_bounds__(BS, 8) k_y_epi(KArgs A, double* part, int cap, CtrlFuse F) {
+__global__ void __launch_bounds__(BS, 8) k_y_epi(KArgs A, double* part, int cap, CtrlFuse F, ShortRows R) {
   pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop) return;
@@ -1607,20 +1687,20 @@ __global__ void __launch_bounds__(BS, 8) k_y_epi(KArgs A, double* part, int cap,
   const uint64_t ps = policy_stream(), pky = policy_keep_frac(A.keep_yh);
   double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A.m; r += gridDim.x * blockDim.x)
-    y_epilogue<H>(A, k, r, ld_hint<H>(A.w + r, ps), acc, ps, pky);
+    y_epilogue<H>(A, k, r, cls_dot(R, r, ld_hint<H>(A.w + r, ps), A.w), acc, ps, pky);
   block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
   fused_ctrl(F);
 }
 
 template <bool H>
-__global__ void __launch_bounds__(BS, 8) k_t_epi(KArgs A, double* part, int cap, CtrlFuse F) {
+__global__ void __launch_bounds__(BS, 8) k_t_epi(KArgs A, double* part, int cap, CtrlFuse F, ShortRows R) {
   pdl_enter();
   const PdcsCtrl* C = A.ctrl;
   if (C->stop || !C->accepted) return;
   const uint64_t ps = policy_stream();
   double acc[GT_N] = {0.0, 0.0, 0.0};
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.nbox; j += gridDim.x * blockDim.x)
-    t_epilogue<H, false>(A, j, ld_hint<H>(A.gth + j, ps), acc, ps);
+    t_epilogue<H, false>(A, j, cls_dot(R, j, ld_hint<H>(A.gth + j, ps), A.gth), acc, ps);
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
   fused_ctrl(F);
 }

@@ -1,0 +1,8 @@
+set -x
+export PYTHONUNBUFFERED=1
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/r2w_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2w_pytest.log
+for c in C2 C3 C4; do
+for t in "" "blkfuse=0"; do
+  PDCS_TUNE="$t" timeout 300 python bench.py --config $c --steps 300 --warmup 20 --no-cpu-baseline --no-e2e --no-ttt-c1 --no-sustained >> gpurun_out/r2w_cfg.jsonl 2>> gpurun_out/r2w_cfg.err
+done
+done

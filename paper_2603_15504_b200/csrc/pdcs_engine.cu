@@ -1518,12 +1518,14 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   const KArgs A = make_args(E);
   const int n = E->n, m = E->m, nnz = E->nnz;
   PhaseTimer T("precondition", s);
+  T.lap("queued work");
   int* rowid = nullptr;
   if (nnz > 0) {
     CK(cudaMallocAsync(&rowid, sizeof(int) * nnz, s));
     k_iota_rows<<<grid_for(m), BS, 0, s>>>(d.d_g_rowptr, m, rowid);
     CKL();
   }
+  T.lap("row ids");
   E->precond_mode = enabled;
   // enabled: 0 identity, 1 Ruiz + PC on this matrix, 2 as-is (d1/d2 = cone
   // scales, values untouched), 3 d1/d2 written by the caller (a shard taking
@@ -1557,6 +1559,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
                                                 d.d_tx1, nnz);
       CKL();
     }
+    T.lap("ruiz rounds");
     if (use_pc) {  // Pock-Chambolle alpha = 1 (scaling.py:92-96)
       k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
       CKL();
@@ -1581,6 +1584,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
     k_clip<<<grid_for(n), BS, 0, s>>>(d.d_d2, n, 1e-8, 1e8);
     CKL();
   }
+  T.lap("pc + clip");
   // G^ = D1 G D2 from the original values, then its transpose by the perm map
   if (nnz > 0) {
     if (enabled == 2) {
@@ -1601,7 +1605,7 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   CKL();
   if (rowid) CK(cudaFreeAsync(rowid, s));
   CK(cudaStreamSynchronize(s));
-  T.lap("ruiz + pc + scale");
+  T.lap("scale + panels");
   return 0;
 }
 

@@ -127,9 +127,9 @@ struct Y {  // y-space vectors of the epilogue
 __global__ void __launch_bounds__(BS, 8) k_xstep(const double* a0, const double* a1, const double* a2,
                                                  const double* a3, const double* a4, const double* a5,
                                                  const double* a6, double* b0, double* b1, double* b2,
-                                                 double* b3, double* xt, double* part) {
+                                                 double* b3, double* xt, double* part, int j0 = 0, int j1 = N) {
   double acc = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+  for (int j = j0 + blockIdx.x * blockDim.x + threadIdx.x; j < j1; j += gridDim.x * blockDim.x) {
     const double x = a0[j], xh = a1[j], xa = a2[j], g = a4[j], gh = a5[j], ga = a6[j];
     const double xn = 0.9 * xh + 0.05 * x + 0.05 * xa, gn = 0.9 * gh + 0.05 * g + 0.05 * ga;
     b0[j] = xn;
@@ -404,6 +404,60 @@ int main(int argc, char** argv) {
   auto xstep = [&]() {
     k_xstep<<<gx, BS>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6], xs[7], xs[8], xs[9], xs[10], xt, part);
   };
+
+  if (argc > 2 && atoi(argv[2]) == 1) {
+    // pipelined x-step / y passes: x-step over column slice p+1 runs while the
+    // pass over panel p gathers (two streams; grids split the SM slots)
+    cudaStream_t s1, s2;
+    CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev(8);
+    for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::vector<int> cuts = {0, N / 3, (int)(2LL * N / 3), N};
+    Panels Q = build(d_col, d_val, cuts);
+    const int P = Q.P;
+    const double fxs[] = {1.0, 0.5, 0.5, 0.25, 0.75, 0.35};
+    const double fps[] = {1.0, 0.5, 1.0, 0.75, 0.5, 1.0};
+    for (int pipe = 0; pipe < 2; ++pipe)
+      for (int vi = 0; vi < 6; ++vi) {
+        if (!pipe && vi) break;
+        const int gxs = std::max(1, (int)(gx * fxs[vi])), gps = std::max(1, (int)(gp * fps[vi]));
+        float best = 1e9;
+        for (int it = 0; it < reps + 2; ++it) {
+          CK(cudaEventRecord(e0, s1));
+          double* win = nullptr;
+          double* bufs[2] = {wA, wB};
+          for (int p = 0; p < P; ++p) {
+            cudaStream_t sx = pipe ? s1 : s2;
+            if (!pipe && p == 0) CK(cudaStreamWaitEvent(s2, e0));
+            k_xstep<<<pipe ? (p == 0 ? gx : gxs) : gx, BS, 0, sx>>>(xs[0], xs[1], xs[2], xs[3], xs[4], xs[5], xs[6],
+                                                                  xs[7], xs[8], xs[9], xs[10], xt, part,
+                                                                  cuts[p], cuts[p + 1]);
+            CK(cudaEventRecord(ev[p], sx));
+          }
+          for (int p = 0; p < P; ++p) {
+            CK(cudaStreamWaitEvent(s2, ev[p]));
+            const int* po = Q.d_po + (size_t)p * M;
+            double* wo = bufs[p & 1];
+            if (p == 0) k_pass<true><<<pipe ? gps : gp, BS, 0, s2>>>(po, Q.d_pci, Q.d_pva, xt, nullptr, wo);
+            else k_pass<false><<<pipe ? gps : gp, BS, 0, s2>>>(po, Q.d_pci, Q.d_pva, xt, win, wo);
+            win = wo;
+          }
+          k_epi<<<ge, BS, 0, s2>>>(win, Yv, part);
+          CK(cudaEventRecord(e2, s2));
+          CK(cudaEventSynchronize(e2));
+          float ms = 0;
+          cudaEventElapsedTime(&ms, e0, e2);
+          if (it >= 2) best = std::min(best, ms);
+        }
+        CK(cudaGetLastError());
+        printf("%s fx %.2f fp %.2f: x-step + 3 passes + epilogue %.4f ms\n", pipe ? "pipelined " : "sequential",
+               fxs[vi], fps[vi], best);
+        fflush(stdout);
+      }
+    free_panels(Q);
+    return 0;
+  }
 
   struct Variant { const char* name; std::vector<double> fr; int order; int split; int mode = 0; int gmode = 0; int tma = 0; };
   // fr: panel width fractions; order 0 = panels 0..P-1, 1 = reversed; split: epilogue in its own kernel

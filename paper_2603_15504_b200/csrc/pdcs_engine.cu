@@ -270,7 +270,7 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   for (size_t i = 0; i < lrows.size(); ++i) {
     const int r = lrows[i], b = lext[i].x, e = lext[i].y;
     lfirst.push_back((int)chunks.size());
-    for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), 0));
+    for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), (int)i));
   }
   lfirst.push_back((int)chunks.size());
   P.n_long = (int)lrows.size();
@@ -280,6 +280,8 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
     CK(cudaMalloc(&P.d_long_first, sizeof(int) * (P.n_long + 1)));
     CK(cudaMalloc(&P.d_chunks, sizeof(int4) * P.n_chunks));
     CK(cudaMalloc(&P.d_chunk_out, sizeof(double) * P.n_chunks));
+    CK(cudaMalloc(&P.d_long_cnt, sizeof(unsigned) * P.n_long));
+    CK(cudaMemsetAsync(P.d_long_cnt, 0, sizeof(unsigned) * P.n_long, s));
     CK(cudaMemcpyAsync(P.d_long_rows, lrows.data(), sizeof(int) * P.n_long, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P.d_long_first, lfirst.data(), sizeof(int) * (P.n_long + 1), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P.d_chunks, chunks.data(), sizeof(int4) * P.n_chunks, cudaMemcpyHostToDevice, s));
@@ -387,6 +389,7 @@ void free_plan(SpmvPlan& P) {
   cudaFree(P.d_long_first);
   cudaFree(P.d_chunks);
   cudaFree(P.d_chunk_out);
+  cudaFree(P.d_long_cnt);
   cudaFree(P.d_tiles);
   P = SpmvPlan();
 }
@@ -396,10 +399,8 @@ int launch_long(const SpmvPlan& P, const double* x, double* y, const PdcsCtrl* c
                 cudaStream_t s) {
   if (P.n_long == 0) return 0;
   k_long_partial<<<grid_for(P.n_chunks, 1), BS, 0, s>>>(P.d_chunks, P.n_chunks, P.colidx, P.val, x,
-                                                        P.d_chunk_out, ctrl, gate);
-  CKL();
-  k_long_final<<<grid_for(P.n_long, 128), 128, 0, s>>>(P.d_long_rows, P.d_long_first, P.n_long,
-                                                       P.d_chunk_out, y, ctrl, gate);
+                                                        P.d_chunk_out, ctrl, gate, P.d_long_first,
+                                                        P.d_long_cnt, y);
   CKL();
   return 0;
 }

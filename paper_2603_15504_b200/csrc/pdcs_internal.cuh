@@ -28,6 +28,7 @@ struct SpmvPlan {
   int* d_long_first = nullptr;    // [n_long + 1] first chunk of each long row
   int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
   double* d_chunk_out = nullptr;  // [n_chunks]
+  unsigned* d_long_cnt = nullptr;  // [n_long] chunks of the row finished (k_long_partial ticket)
   int grid = 1;                   // CTAs of the short-row kernel
   // row classes of a mixed-length matrix (class split): the rows of more than
   // CLS_SHORT entries (cls_vw lanes per row); the epilogue sums the others

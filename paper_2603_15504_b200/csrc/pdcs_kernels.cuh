@@ -192,7 +192,7 @@ __device__ __forceinline__ double row_dot(const int* __restrict__ rp, const int*
 }
 
 // Generic SpMV for short rows; long rows are already in y (written by
-// k_long_final) and are left untouched.
+// k_long_partial) and are left untouched.
 template <int VW>
 __global__ void __launch_bounds__(BS) k_spmv(int nrows, const int* __restrict__ rp,
                                              const int* __restrict__ ci,
@@ -212,41 +212,52 @@ __global__ void __launch_bounds__(BS) k_spmv(int nrows, const int* __restrict__ 
   }
 }
 
+// Chunks of the long rows, one CTA reduction each; the last chunk of a row
+// to finish (per-row ticket) adds the row's chunk sums in chunk order and
+// writes y[row] -- no second launch, and the sum order is fixed.
+// q = (row, begin, end, index of the row in the long-row list).
 __global__ void k_long_partial(const int4* __restrict__ ch, int nch, const int* __restrict__ ci,
                                const double* __restrict__ va, const double* __restrict__ x,
-                               double* out, const PdcsCtrl* ctrl, int gate) {
+                               double* out, const PdcsCtrl* ctrl, int gate, const int* __restrict__ first,
+                               unsigned* cnt, double* y) {
   if (gated(ctrl, gate)) return;
   __shared__ double sh[33];
   CtaGrp g(sh);
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     const int4 q = ch[c];
-    // four independent accumulators keep four gathers in flight per thread
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    // eight independent gathers in flight per thread: the column loads of a
+    // group first, then the gathers (the chain ci -> x is latency bound)
+    constexpr int U = 8;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     const int bd = blockDim.x;
     int j = q.y + threadIdx.x;
-    for (; j + 3 * bd < q.z; j += 4 * bd) {
-      const int c0 = __ldg(ci + j), c1 = __ldg(ci + j + bd), c2 = __ldg(ci + j + 2 * bd),
-                c3 = __ldg(ci + j + 3 * bd);
-      s0 += __ldg(va + j) * __ldg(x + c0);
-      s1 += __ldg(va + j + bd) * __ldg(x + c1);
-      s2 += __ldg(va + j + 2 * bd) * __ldg(x + c2);
-      s3 += __ldg(va + j + 3 * bd) * __ldg(x + c3);
+    for (; j + (U - 1) * bd < q.z; j += U * bd) {
+      int cc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cc[u] = __ldg(ci + j + u * bd);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u & 3] += __ldg(va + j + u * bd) * __ldg(x + cc[u]);
     }
-    for (; j < q.z; j += bd) s0 += __ldg(va + j) * __ldg(x + __ldg(ci + j));
-    const double s = g.sum((s0 + s1) + (s2 + s3));
-    if (threadIdx.x == 0) out[c] = s;
+    for (; j < q.z; j += bd) acc[0] += __ldg(va + j) * __ldg(x + __ldg(ci + j));
+    const double s = g.sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+    if (threadIdx.x == 0) {
+      out[c] = s;
+      const int i = q.w, f = first[i], nc = first[i + 1] - f;
+      if (nc == 1) {
+        y[q.x] = s;
+      } else {
+        __threadfence();
+        if (atomicAdd(cnt + i, 1u) == (unsigned)(nc - 1)) {
+          __threadfence();
+          double t = 0.0;
+          for (int k = f; k < f + nc; ++k) t += __ldcg(out + k);
+          y[q.x] = t;
+          cnt[i] = 0u;
+        }
+      }
+    }
+    __syncthreads();
   }
-}
-
-__global__ void k_long_final(const int* __restrict__ rows, const int* __restrict__ first, int nl,
-                             const double* __restrict__ part, double* y, const PdcsCtrl* ctrl,
-                             int gate) {
-  if (gated(ctrl, gate)) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nl) return;
-  double s = 0.0;
-  for (int c = first[i]; c < first[i + 1]; ++c) s += part[c];
-  y[rows[i]] = s;
 }
 
 // Panel build: entries per (panel, row); long rows get none.

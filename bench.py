@@ -51,6 +51,9 @@ WORKLOADS = {
             lambda I: I.entropy_max_primal()),
     "C2p": ("C2p: group_regression_primal 10k PRIMAL SOC(11) blocks (rescaled), n=155k m=100k",
             lambda I: I.group_regression_primal()),
+    # C5's pattern at 1/10 (single-panel SpMVs; launch-variant sweeps only)
+    "C5s": ("C5s: lp_large m=1,000,000 n=2,000,000 5 nnz/row (C5 pattern at 1/10)",
+            lambda I: I.lp_large(m=1_000_000, n=2_000_000)),
 }
 
 

@@ -259,8 +259,17 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
     }
     CK(cudaFreeAsync(st, s));
   }
-  // entries per long-row chunk (one CTA reduction each); PDCS_TUNE=chunk=N overrides
-  int chunk = 8192;
+  // entries per long-row chunk (one CTA reduction each): the long rows' entries
+  // spread over one wave of k_long_partial (8 CTAs per SM; a partial second
+  // wave cost C4 ~8%), each row cut into equal chunks; PDCS_TUNE=chunk=N fixes N
+  long long total = 0;
+  for (const int2& x : lext) total += x.y - x.x;
+  int dev = 0, nsm_ = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, dev);
+  const long long resident = 8LL * nsm_;
+  const long long slots = std::max<long long>(resident - (long long)lrows.size(), resident / 2);
+  long long chunk = std::max<long long>(2048, (total + slots - 1) / slots);
   if (const char* env = getenv("PDCS_TUNE")) {
     const char* p = strstr(env, "chunk=");
     if (p && (p == env || p[-1] == ',')) chunk = std::max(256, atoi(p + 6));
@@ -269,8 +278,10 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
   std::vector<int4> chunks;
   for (size_t i = 0; i < lrows.size(); ++i) {
     const int r = lrows[i], b = lext[i].x, e = lext[i].y;
+    const long long len = e - b, nc = (len + chunk - 1) / chunk, cl = (len + nc - 1) / nc;
     lfirst.push_back((int)chunks.size());
-    for (int j = b; j < e; j += chunk) chunks.push_back(make_int4(r, j, std::min(e, j + chunk), (int)i));
+    for (long long j = b; j < e; j += cl)
+      chunks.push_back(make_int4(r, (int)j, (int)std::min<long long>(e, j + cl), (int)i));
   }
   lfirst.push_back((int)chunks.size());
   P.n_long = (int)lrows.size();
@@ -285,6 +296,8 @@ int build_plan(SpmvPlan& P, int nrows, int ncols, int nnz, const int* d_rp, cons
     CK(cudaMemcpyAsync(P.d_long_rows, lrows.data(), sizeof(int) * P.n_long, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P.d_long_first, lfirst.data(), sizeof(int) * (P.n_long + 1), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(P.d_chunks, chunks.data(), sizeof(int4) * P.n_chunks, cudaMemcpyHostToDevice, s));
+    k_chunk_dense<<<std::min(P.n_chunks, MAX_GRID), BS, 0, s>>>(P.d_chunks, P.n_chunks, d_ci);
+    CKL();
     CK(cudaStreamSynchronize(s));
   }
   P.grid = grid_for(nrows, BS / P.vw);
@@ -359,6 +372,7 @@ int build_classes(SpmvPlan& P, cudaStream_t s, int nsm) {
   CK(cudaFreeAsync(st, s));
   P.n_cls_short = (int)h[2];
   P.n_cls_long = (int)h[3];
+  P.nnz_cls_long = (long long)P.nnz - (long long)h[0];
   const double mean_long = P.n_cls_long ? (double)(P.nnz - (long long)h[0]) / P.n_cls_long : 0.0;
   // lanes per long row: about 4-8 entries per lane (PDCS_TUNE cls_vw=8|16|32)
   const int vw = (int)tune_env("cls_vw", mean_long <= 64.0 ? 8.0 : (mean_long <= 160.0 ? 16.0 : 32.0));
@@ -1371,24 +1385,34 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
                                                 : fit((const void*)k_t_epi<false>, nx));
     }
-    // class split (mixed row lengths, one panel, no chunked long rows; PDCS_TUNE
-    // cls=0 off): rows of > 6 entries 8/16/32 lanes per row, then the streaming
-    // epilogue, which sums the short rows itself; replaces the tiled / 8-lane step of C2-class matrices
+    // class split (one panel, no chunked long rows; PDCS_TUNE cls=0 off): rows of
+    // > 6 entries 8/16/32 lanes per row, then the streaming epilogue, which sums
+    // the short rows itself.  Taken when the long class holds at least half of
+    // the entries (cls_frac): C2's G and G^T (+7%), C4's G^T of 42-entry rows;
+    // mostly-short matrices keep the fused lane kernels (C5's pattern at 1/10:
+    // 6.3k vs 6.8k it/s with the class split of its G^T)
     {
       const bool cls_on = tune("cls", 1.0) > 0.0;
-      const double cls_nnz = tune("cls_nnz", (double)(1 << 20));
-      auto mixed = [&](const SpmvPlan& P, const PanelPlan& Q) {
-        return cls_on && !E->split && P.n_long == 0 && Q.np == 1 && P.len_cv > 0.5 && (double)d.nnz >= cls_nnz;
+      const double cls_nnz = tune("cls_nnz", (double)(1 << 20)), cls_frac = tune("cls_frac", 0.5);
+      auto classes = [&](SpmvPlan& P, const PanelPlan& Q, bool& on) {
+        if (!cls_on || E->split || P.n_long != 0 || Q.np != 1 || (double)d.nnz < cls_nnz || P.nnz == 0) return 0;
+        if (build_classes(P, s, nsm)) return 1;
+        if ((double)P.nnz_cls_long >= cls_frac * (double)P.nnz) {
+          on = true;
+        } else {
+          cudaFree(P.d_cls_long);
+          P.d_cls_long = nullptr;
+          P.n_cls_long = 0;
+        }
+        return 0;
       };
-      if (mixed(E->G, E->PG)) {
-        if (build_classes(E->G, s, nsm)) return fail(1);
-        E->cls_y = true;
+      if (classes(E->G, E->PG, E->cls_y)) return fail(1);
+      if (classes(E->GT, E->PGT, E->cls_t)) return fail(1);
+      if (E->cls_y) {
         const int ny = grid_for(d.m, BS, 1 << 30);
         E->G.grid = grid_per_sm("gy", ny, fit((const void*)k_y_epi<false>, ny));
       }
-      if (mixed(E->GT, E->PGT)) {
-        if (build_classes(E->GT, s, nsm)) return fail(1);
-        E->cls_t = true;
+      if (E->cls_t) {
         const int nx = grid_for(d.n, BS, 1 << 30);
         E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
                                                   : fit((const void*)k_t_epi<false>, nx));

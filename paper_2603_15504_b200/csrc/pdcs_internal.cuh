@@ -26,7 +26,7 @@ struct SpmvPlan {
   int n_long = 0, n_chunks = 0;
   int* d_long_rows = nullptr;     // [n_long]
   int* d_long_first = nullptr;    // [n_long + 1] first chunk of each long row
-  int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, 0)
+  int4* d_chunks = nullptr;       // [n_chunks] (row, begin, end, long-row index | LONG_DENSE)
   double* d_chunk_out = nullptr;  // [n_chunks]
   unsigned* d_long_cnt = nullptr;  // [n_long] chunks of the row finished (k_long_partial ticket)
   int grid = 1;                   // CTAs of the short-row kernel
@@ -34,6 +34,7 @@ struct SpmvPlan {
   // CLS_SHORT entries (cls_vw lanes per row); the epilogue sums the others
   int* d_cls_long = nullptr;
   int n_cls_short = 0, n_cls_long = 0, cls_vw = 8;
+  long long nnz_cls_long = 0;
   int cls_grid_l = 1;
   int pass_grid = 1;              // CTAs of the panel partial-sum passes (k_lane_pass)
   int* d_tiles = nullptr;         // [ntiles + 1] CSR-stream tile boundaries (rows)

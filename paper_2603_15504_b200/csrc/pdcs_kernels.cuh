@@ -215,8 +215,23 @@ __global__ void __launch_bounds__(BS) k_spmv(int nrows, const int* __restrict__ 
 // Chunks of the long rows, one CTA reduction each; the last chunk of a row
 // to finish (per-row ticket) adds the row's chunk sums in chunk order and
 // writes y[row] -- no second launch, and the sum order is fixed.
-// q = (row, begin, end, index of the row in the long-row list).
-__global__ void k_long_partial(const int4* __restrict__ ch, int nch, const int* __restrict__ ci,
+// q = (row, begin, end, index of the row in the long-row list | LONG_DENSE
+// when the chunk's columns are consecutive: C4's dense factor rows read no
+// column indices and stream x).
+constexpr int LONG_DENSE = 1 << 30;
+__global__ void k_chunk_dense(int4* ch, int nch, const int* __restrict__ ci) {
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    const int4 q = ch[c];
+    const int c0 = ci[q.y];
+    int ok = 1;
+    for (int j = q.y + threadIdx.x; j < q.z; j += blockDim.x) ok &= ci[j] == c0 + (j - q.y);
+    ok = __syncthreads_and(ok);
+    if (threadIdx.x == 0 && ok) ch[c].w = q.w | LONG_DENSE;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(BS, 8) k_long_partial(const int4* __restrict__ ch, int nch, const int* __restrict__ ci,
                                const double* __restrict__ va, const double* __restrict__ x,
                                double* out, const PdcsCtrl* ctrl, int gate, const int* __restrict__ first,
                                unsigned* cnt, double* y) {
@@ -231,18 +246,27 @@ __global__ void k_long_partial(const int4* __restrict__ ch, int nch, const int* 
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     const int bd = blockDim.x;
     int j = q.y + threadIdx.x;
-    for (; j + (U - 1) * bd < q.z; j += U * bd) {
-      int cc[U];
+    if (q.w & LONG_DENSE) {
+      const double* xs = x + (__ldg(ci + q.y) - q.y);  // x index = column of j
+      for (; j + (U - 1) * bd < q.z; j += U * bd) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) cc[u] = __ldg(ci + j + u * bd);
+        for (int u = 0; u < U; ++u) acc[u & 3] += __ldg(va + j + u * bd) * __ldg(xs + j + u * bd);
+      }
+      for (; j < q.z; j += bd) acc[0] += __ldg(va + j) * __ldg(xs + j);
+    } else {
+      for (; j + (U - 1) * bd < q.z; j += U * bd) {
+        int cc[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc[u & 3] += __ldg(va + j + u * bd) * __ldg(x + cc[u]);
+        for (int u = 0; u < U; ++u) cc[u] = __ldg(ci + j + u * bd);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u & 3] += __ldg(va + j + u * bd) * __ldg(x + cc[u]);
+      }
+      for (; j < q.z; j += bd) acc[0] += __ldg(va + j) * __ldg(x + __ldg(ci + j));
     }
-    for (; j < q.z; j += bd) acc[0] += __ldg(va + j) * __ldg(x + __ldg(ci + j));
     const double s = g.sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
     if (threadIdx.x == 0) {
       out[c] = s;
-      const int i = q.w, f = first[i], nc = first[i + 1] - f;
+      const int i = q.w & (LONG_DENSE - 1), f = first[i], nc = first[i + 1] - f;
       if (nc == 1) {
         y[q.x] = s;
       } else {
@@ -1395,6 +1419,15 @@ __device__ __forceinline__ double cls_dot(const ShortRows& R, int r, double w, d
   return s;
 }
 
+// Class split of G^T: the columns past the box (primal cone blocks) are
+// projected by the block kernels after the epilogue, which read G^T y_hat
+// from gth -- their short rows are summed and stored here.
+__device__ __forceinline__ void cls_cone_cols(const KArgs& A, const ShortRows& R) {
+  if (R.rp == nullptr) return;
+  for (int j = A.nbox + blockIdx.x * blockDim.x + threadIdx.x; j < A.n; j += gridDim.x * blockDim.x)
+    cls_dot(R, j, 0.0, A.gth);
+}
+
 // ---- 16-byte (double2) streaming variants of the step epilogues -------------
 // The same per-element arithmetic as k_step_x / y_epilogue / t_epilogue, with
 // every stream moved as aligned pairs (one 16-byte load or store per two
@@ -1618,6 +1651,7 @@ __global__ void __launch_bounds__(BS, 5) k_t_epi2(KArgs A, double* part, int cap
     const int j = A.nbox - 1;
     t_elem(A, cls_dot(R, j, A.gth[j], A.gth), A.c[j], A.ub == 1 ? A.d2[j] : 1.0, acc);
   }
+  cls_cone_cols(A, R);
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
   fused_ctrl(F);
 }
@@ -1712,6 +1746,7 @@ __global__ void __launch_bounds__(BS, 8) k_t_epi(KArgs A, double* part, int cap,
   double acc[GT_N] = {0.0, 0.0, 0.0};
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < A.nbox; j += gridDim.x * blockDim.x)
     t_epilogue<H, false>(A, j, cls_dot(R, j, ld_hint<H>(A.gth + j, ps), A.gth), acc, ps);
+  cls_cone_cols(A, R);
   block_store_mask<GT_N>(acc, 0u, part, cap, blockIdx.x);
   fused_ctrl(F);
 }

@@ -43,6 +43,19 @@ def _mixed():
     return instances.group_robust_regression(ngroups=300, gsize=10, q=400, nnz_per_row=40, seed=5)
 
 
+def _primal_soc():
+    from paper_2603_15504_b200 import instances
+
+    # primal SOC(11) blocks past the box: G^T rows of the cone columns are short
+    return instances.group_regression_primal(ngroups=200, gsize=10, q=300, nnz_per_row=30, seed=4)
+
+
+def _primal_exp():
+    from paper_2603_15504_b200 import instances
+
+    return instances.entropy_max_primal(nblk=3000, p=40, nnz_per_col=3, seed=3)
+
+
 def _lp():
     from paper_2603_15504_b200 import instances
 
@@ -50,11 +63,16 @@ def _lp():
 
 
 CASES = [
-    ("mixed", "cls_nnz=0"),              # class split: short rows thread/row, long rows 8/32 lanes
+    ("mixed", "cls_nnz=0,cls_frac=0"),   # class split: short rows thread/row, long rows 8/32 lanes
     ("mixed", "cls=0"),                  # tiled / 8-lane step kernels
+    ("mixed", "cls_nnz=0,cls_frac=0,cls_vw=32"),    # class split, 32 lanes per long row
+    ("primal_soc", "cls_nnz=0,cls_frac=0"),  # class split with primal cone columns after the box
+    ("primal_exp", "cls_nnz=0,cls_frac=0"),
+    ("primal_soc", "cls=0"),
+    ("lp", "cls_nnz=0,cls_frac=0"),       # class split on uniform short rows (all in the epilogue)
     ("mixed", "cls=0,tile=1"),           # tiled step kernels forced
     ("mixed", "cls=0,tile=0"),           # lane-mapped step kernels
-    ("mixed", "cls_nnz=0,vec=0"),        # class split with scalar epilogues
+    ("mixed", "cls_nnz=0,cls_frac=0,vec=0"),        # class split with scalar epilogues
     ("lp", "py=3,pt=2,split=1"),         # column panels: gather-only passes + streaming epilogues
     ("lp", "py=3,pt=2,split=0"),         # column panels, fused step kernels
     ("lp", "py=3,pt=2,split=1,hs=0,vec=0"),  # split without L2 hints / double2 epilogues
@@ -67,7 +85,7 @@ CASES = [
 def test_variant_trajectory_matches_oracle(shape, tune, monkeypatch):
     import paper_2603_15504_b200 as P
 
-    p = _mixed() if shape == "mixed" else _lp()
+    p = {"mixed": _mixed, "lp": _lp, "primal_soc": _primal_soc, "primal_exp": _primal_exp}[shape]()
     kb = (1, 2, 5, 10)
     dev, orc = _trajectory(P, p, dict(max_iter=10, rel_tol=1e-14, abs_tol=1e-14), kb, tune, monkeypatch)
     assert sorted(dev) == sorted(orc) and dev, (sorted(dev), sorted(orc))

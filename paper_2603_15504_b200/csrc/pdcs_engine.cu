@@ -376,7 +376,7 @@ int build_classes(SpmvPlan& P, cudaStream_t s, int nsm) {
   const double mean_long = P.n_cls_long ? (double)(P.nnz - (long long)h[0]) / P.n_cls_long : 0.0;
   // lanes per long row: about 4-8 entries per lane (PDCS_TUNE cls_vw=8|16|32)
   const int vw = (int)tune_env("cls_vw", mean_long <= 64.0 ? 8.0 : (mean_long <= 160.0 ? 16.0 : 32.0));
-  P.cls_vw = vw == 32 ? 32 : (vw == 16 ? 16 : 8);
+  P.cls_vw = vw == 32 ? 32 : (vw == 16 ? 16 : (vw == 4 ? 4 : 8));
   CK(cudaMalloc(&P.d_cls_long, sizeof(int) * std::max(P.n_cls_long, 1)));
   int* num = nullptr;
   CK(cudaMallocAsync(&num, sizeof(int), s));
@@ -390,8 +390,10 @@ int build_classes(SpmvPlan& P, cudaStream_t s, int nsm) {
   CK(cudaFreeAsync(num, s));
   CK(cudaStreamSynchronize(s));
   int occ = 1;
-  const void* fn = P.cls_vw == 32 ? (const void*)k_rows_pass<32>
-                                  : (P.cls_vw == 16 ? (const void*)k_rows_pass<16> : (const void*)k_rows_pass<8>);
+  const void* fn = P.cls_vw == 32   ? (const void*)k_rows_pass<32>
+                   : P.cls_vw == 16 ? (const void*)k_rows_pass<16>
+                   : P.cls_vw == 4  ? (const void*)k_rows_pass<4>
+                                    : (const void*)k_rows_pass<8>;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BS, 0) != cudaSuccess || occ < 1) occ = 1;
   P.cls_grid_l = std::max(1, std::min(grid_for(P.n_cls_long, BS / P.cls_vw, 1 << 30), occ * nsm));
   return 0;
@@ -753,7 +755,10 @@ int launch_gt_partial(Engine* E) {
 int class_pass(Engine* E, const SpmvPlan& P, const double* x, double* out, int gate) {
   if (!P.n_cls_long) return 0;
   const PdcsCtrl* c = E->d_ctrl;
-  auto fn = P.cls_vw == 32 ? k_rows_pass<32> : P.cls_vw == 16 ? k_rows_pass<16> : k_rows_pass<8>;
+  auto fn = P.cls_vw == 32 ? k_rows_pass<32>
+            : P.cls_vw == 16 ? k_rows_pass<16>
+            : P.cls_vw == 4  ? k_rows_pass<4>
+                             : k_rows_pass<8>;
   CK(launch_step(use_pdl(E), fn, P.cls_grid_l, E->stream, (const int*)P.d_cls_long, P.n_cls_long,
                  P.rowptr, P.colidx, (const double*)P.val, x, out, c, gate));
   CKL();

@@ -1852,6 +1852,45 @@ __device__ __forceinline__ void cta_sum_rows(const double* p, int cap, int n, do
 
 // Line-search controller (engine.py:183-243), run by one whole CTA.
 // yred (sharded mode): the y-space sums already all-reduced across ranks.
+// The line-search sums of both spaces in one pass: the x- and y-space partial
+// rows are loaded together and share one pair of barriers (the controller
+// kernel is latency bound: two sequential reductions cost a round trip each).
+template <int NA, int NB>
+__device__ __forceinline__ void cta_sum_rows2(const double* pa, int capa, int na, const double* pb, int capb,
+                                              int nb, double (&oa)[NA], double (&ob)[NB]) {
+  __shared__ double sh[NA + NB][32];
+  double t[NA + NB];
+#pragma unroll
+  for (int q = 0; q < NA + NB; ++q) t[q] = 0.0;
+  const int bd = blockDim.x, n = na > nb ? na : nb;
+  for (int s0 = threadIdx.x; s0 < n; s0 += bd) {
+    if (s0 < na) {
+#pragma unroll
+      for (int q = 0; q < NA; ++q) t[q] += __ldcg(pa + (size_t)q * capa + s0);
+    }
+    if (s0 < nb) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) t[NA + q] += __ldcg(pb + (size_t)q * capb + s0);
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NA + NB; ++q) {
+    for (int off = 16; off > 0; off >>= 1) t[q] += __shfl_down_sync(0xffffffffu, t[q], off);
+    if (lane == 0) sh[q][wid] = t[q];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NA + NB; ++q) {
+      double v = lane < nw ? sh[q][lane] : 0.0;
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+      if (q < NA) oa[q < NA ? q : 0] = v;
+      else ob[q >= NA ? q - NA : 0] = v;
+    }
+  }
+}
+
 template <int U>
 __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                              int capY, double* red, const double* yred) {
@@ -1862,8 +1901,7 @@ __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const d
 #pragma unroll
     for (int q = 0; q < GX_N; ++q) sx[q] = yred[GY_N + q];
   } else {
-    cta_sum_rows<GX_N, U>(partX, capX, capX, sx);
-    cta_sum_rows<GY_N, U>(partY, capY, capY, sy);
+    cta_sum_rows2<GX_N, GY_N>(partX, capX, capX, partY, capY, capY, sx, sy);
   }
   if (threadIdx.x != 0) return;
   const double xx = sx[GX_XX], dxdx = sx[GX_DXDX], cx = sx[GX_CX];
@@ -1923,10 +1961,29 @@ __device__ void ctrl_ls_body(PdcsCtrl* C, const double* partX, int capX, const d
   }
 }
 
+// The standalone controllers work on a shared-memory copy of the control
+// block (one parallel load and store instead of thread 0's chain of
+// dependent global read-modify-writes).
+__device__ __forceinline__ void ctrl_to_smem(PdcsCtrl* sc, const PdcsCtrl* C) {
+  constexpr int NW = sizeof(PdcsCtrl) / sizeof(long long);
+  for (int i = threadIdx.x; i < NW; i += blockDim.x)
+    reinterpret_cast<long long*>(sc)[i] = reinterpret_cast<const long long*>(C)[i];
+  __syncthreads();
+}
+__device__ __forceinline__ void ctrl_from_smem(PdcsCtrl* C, const PdcsCtrl* sc) {
+  constexpr int NW = sizeof(PdcsCtrl) / sizeof(long long);
+  __syncthreads();
+  for (int i = threadIdx.x; i < NW; i += blockDim.x)
+    reinterpret_cast<long long*>(C)[i] = reinterpret_cast<const long long*>(sc)[i];
+}
+
 __global__ void k_ctrl_ls(PdcsCtrl* C, const double* partX, int capX, const double* partY,
                           int capY, double* red, const double* yred) {
-  if (C->stop) return;
-  ctrl_ls_body<4>(C, partX, capX, partY, capY, red, yred);
+  __shared__ PdcsCtrl sc;
+  ctrl_to_smem(&sc, C);
+  if (sc.stop) return;
+  ctrl_ls_body<4>(&sc, partX, capX, partY, capY, red, yred);
+  ctrl_from_smem(C, &sc);
 }
 
 // Reflection parameter, Halpern coefficients, averaging weight and the stop
@@ -2004,8 +2061,11 @@ __global__ void k_err_to_double(const int* err, double* out) { *out = (double)*e
 
 __global__ void k_ctrl_beta(PdcsCtrl* C, const double* partT, int capT, const double* red,
                             const int* err, const double* tred) {
-  if (C->stop || !C->accepted) return;
-  ctrl_beta_body<4>(C, partT, capT, red, err, tred);
+  __shared__ PdcsCtrl sc;
+  ctrl_to_smem(&sc, C);
+  if (sc.stop || !sc.accepted) return;
+  ctrl_beta_body<4>(&sc, partT, capT, red, err, tred);
+  ctrl_from_smem(C, &sc);
 }
 
 // Controller folded into the last CTA of the kernel that writes the final

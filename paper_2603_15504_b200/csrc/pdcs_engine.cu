@@ -543,7 +543,14 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
   slot += T.g_thread;
   base += T.n_thread;
   if (T.n_half) {
-    k_blk_half<OP><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
+    // register budget of the step half-warp blocks: 3 CTAs per SM (80 registers)
+    // measured best on C2 (PDCS_TUNE halfminb=1|3|4; profiles/r02_sweeps.txt)
+    if (OP != OP_PROJECT && T.half_minb == 4)
+      k_blk_half<OP, 4><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
+    else if (OP != OP_PROJECT && T.half_minb == 3)
+      k_blk_half<OP, 3><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
+    else
+      k_blk_half<OP><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
     CKL();
   }
   slot += T.g_half;
@@ -1217,6 +1224,8 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc)) return fail(1);
   E->xblocks = xb;
   E->has_xblocks = E->tabX.total() > 0;
+  E->tabY.half_minb = (int)tune_env("halfminb", 3.0);
+  E->tabX.half_minb = (int)tune_env("xhalfminb", 3.0);
   if (E->tabY.n_exp) {  // Newton warm starts of the dual exp blocks, NaN = cold
     const size_t cnt = 2 * (size_t)E->tabY.n_exp;
     if (cudaMalloc(&E->d_exp_rho, sizeof(double) * cnt) != cudaSuccess) return fail(1);

@@ -786,8 +786,8 @@ __global__ void __launch_bounds__(BS) k_blk_thread(const PdcsBlock* tab, int nb,
 
 // Small blocks (THREAD_CLASS_MAX < dim <= HALF_CLASS_MAX): 16 lanes per
 // block, two blocks per warp.
-template <int OP>
-__global__ void __launch_bounds__(BS) k_blk_half(const PdcsBlock* tab, int nb, KArgs A,
+template <int OP, int MINB = 1>
+__global__ void __launch_bounds__(BS, MINB) k_blk_half(const PdcsBlock* tab, int nb, KArgs A,
                                                  BlkParams P, double* part, int cap, int slot0,
                                                  int gate) {
   if (gated(A.ctrl, gate)) return;

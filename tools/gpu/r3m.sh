@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+for t in "" "xhalfminb=3" "xhalfminb=4"; do
+  PDCS_TUNE="$t" timeout 300 python bench.py --config C2p --steps 1000 --warmup 20 --no-cpu-baseline --no-e2e --no-ttt-c1 --no-sustained >> gpurun_out/r3m_cfg.jsonl 2>> gpurun_out/r3m_cfg.err
+done
+PDCS_TUNE="" timeout 300 python bench.py --config C2 --steps 1000 --warmup 20 --no-cpu-baseline --no-e2e --no-ttt-c1 --no-sustained >> gpurun_out/r3m_cfg.jsonl 2>> gpurun_out/r3m_cfg.err

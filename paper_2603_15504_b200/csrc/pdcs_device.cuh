@@ -253,9 +253,21 @@ __device__ inline bool dual_exp_member(double u, double v, double w) {
   return u * log(-u / w) - u + v >= 0.0;
 }
 
+// exp(rho) and exp(-rho) for the root search's function evaluations: the
+// second as the correctly rounded reciprocal of the first while both are
+// normal (|rho| < 700), one exp instead of two -- the exp calls are the
+// largest share of the exp-cone kernel's instructions (ncu source page,
+// profiles/r02_sweeps.txt).  The root itself is then tested and used
+// through exp_from_rho, which keeps both exponentials as the reference has.
+__device__ __forceinline__ void exp_pair(double rho, double& ep, double& en) {
+  ep = exp_guard(rho);
+  en = fabs(rho) < 700.0 ? __drcp_rn(ep) : exp_guard(-rho);
+}
+
 __device__ inline double exp_h(double r, double s, double t, double rho) {
   double qd = rho * (rho - 1.0) + 1.0;
-  double ep = exp_guard(rho), en = exp_guard(-rho);
+  double ep, en;
+  exp_pair(rho, ep, en);
   double ca = (rho - 1.0) * r + s, cb = r - rho * s;
   double t1 = (isfinite(ep) || ca != 0.0) ? ca * ep : 0.0;
   double t2 = (isfinite(en) || cb != 0.0) ? cb * en : 0.0;
@@ -265,7 +277,8 @@ __device__ inline double exp_h(double r, double s, double t, double rho) {
 // exp_h and its derivative at the same rho, sharing the two exponentials
 // (the Newton step needs both).
 __device__ inline void exp_hdh(double r, double s, double t, double rho, double& f, double& df) {
-  const double ep = exp_guard(rho), en = exp_guard(-rho);
+  double ep, en;
+  exp_pair(rho, ep, en);
   const double qd = rho * (rho - 1.0) + 1.0;
   const double ca = (rho - 1.0) * r + s, cb = r - rho * s;
   const double t1 = (isfinite(ep) || ca != 0.0) ? ca * ep : 0.0;

@@ -775,6 +775,14 @@ int class_pass(Engine* E, const SpmvPlan& P, const double* x, double* out, int g
 int class_y(Engine* E, const KArgs& A) {
   if (class_pass(E, E->G, E->d.d_xt, E->d.d_w, 1)) return 1;
   const ShortRows R{E->G.rowptr, E->G.colidx, E->G.val, E->d.d_xt};
+  if (E->yblk_fused) {
+    const BlockTable& T = E->tabY;
+    const PdcsBlock* half = T.d_all + T.n_exp + T.n_thread;
+    CK(launch_step(use_pdl(E), k_y_epi_blk<3>, E->G.grid, E->stream, A, E->d_partY, E->capY, R, half, T.n_half,
+                   E->yblk_ga));
+    CKL();
+    return 0;
+  }
   CK(launch_step(use_pdl(E), k_y_epi<false>, E->G.grid, E->stream, A, E->d_partY, E->capY, fuse_ls(E), R));
   CKL();
   return 0;
@@ -970,7 +978,8 @@ int launch_slot(Engine* E) {
   rc = launch_step_y(E, A);
   if (rc) return 1;
   mark(s, "step_y_spmv");
-  const bool yblk = E->has_yblocks && !E->soc_tile;  // else projected inside the tiled y-step
+  // else projected inside the tiled y-step (soc_tile) or the class-split epilogue (yblk_fused)
+  const bool yblk = E->has_yblocks && !E->soc_tile && !E->yblk_fused;
   if (yblk && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s)) return 1;
   if (yblk) mark(s, "blocks_y");
   if (E->comm) {
@@ -1425,6 +1434,23 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
       if (E->cls_y) {
         const int ny = grid_for(d.m, BS, 1 << 30);
         E->G.grid = grid_per_sm("gy", ny, fit((const void*)k_y_epi<false>, ny));
+        // dual cone blocks all of the half-warp class (C2's SOC(11)): projected inside the
+        // epilogue kernel.  Opt-in (PDCS_TUNE yblkfuse=1): measured equal on C2 (9.5-9.8k vs
+        // 9.6k it/s; profiles/r02_sweeps.txt) -- the block work, not the launch, is the cost
+        const BlockTable& T = E->tabY;
+        if (tune("yblkfuse", 0.0) > 0.0 && T.n_half > 0 && T.n_half == T.total() && T.n_giant == 0) {
+          int occ = 1;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_y_epi_blk<3>, BS, 0);
+          const int slots = std::max(2, occ * nsm);
+          const int need_a = std::max(1, grid_for(d.m_elem, BS, 1 << 30));
+          const int need_b = std::max(1, grid_for((long long)T.n_half * 16, BS, 1 << 30));
+          // one wave, the SM slots split in proportion to the two parts' threads
+          int ga = (int)std::max(1LL, std::min<long long>(need_a, (long long)slots * need_a / (need_a + need_b)));
+          int gb = std::max(1, std::min(need_b, slots - ga));
+          E->yblk_fused = true;
+          E->yblk_ga = ga;
+          E->G.grid = ga + gb;
+        }
       }
       if (E->cls_t) {
         const int nx = grid_for(d.n, BS, 1 << 30);

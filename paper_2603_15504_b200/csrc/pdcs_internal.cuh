@@ -136,7 +136,9 @@ struct Engine {
   bool split = false;     // split step SpMVs: gather-only panel passes + streaming epilogues
   bool soc_tile = false;  // dual SOC blocks projected inside the tiled y-step (d_rowhead)
   bool vec = false;       // 16-byte streaming epilogues of the split step
-  bool cls_y = false, cls_t = false;  // class-split step SpMVs (mixed row lengths)
+  bool cls_y = false, cls_t = false;
+  bool yblk_fused = false;  // half-warp dual blocks projected in the class-split epilogue (k_y_epi_blk)
+  int yblk_ga = 1;          // its CTAs for the elementwise rows (the rest take the blocks)  // class-split step SpMVs (mixed row lengths)
   bool persist = false;   // small instances: one cooperative launch runs all trials (k_persist)
   int pgrid = 0;          // its grid (one CTA per SM)
   double *d_pX = nullptr, *d_pY = nullptr, *d_pT = nullptr;  // its partial slots [NQ][pgrid]

@@ -1737,6 +1737,45 @@ __global__ void __launch_bounds__(BS, 8) k_y_epi(KArgs A, double* part, int cap,
   fused_ctrl(F);
 }
 
+// Class-split y-step epilogue fused with the dual cone blocks of <= 16 rows
+// (C2's SOC(11)): CTAs [0, ga) stream the elementwise rows; the others give
+// each block to a 16-lane group, which finishes the epilogue of the block's
+// rows (v into yh, the product into w, gx_hat) and projects the block right
+// away (do_block) -- the block kernel's launch and its second pass over the
+// block rows go away, and a block's rows are written and read by one group.
+template <int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_y_epi_blk(KArgs A, double* part, int cap, ShortRows R,
+                                                        const PdcsBlock* tab, int nb, int ga) {
+  pdl_enter();
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ YCoef ks;
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if ((int)blockIdx.x < ga) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < A.m_elem; r += ga * blockDim.x)
+      y_epilogue<false>(A, k, r, cls_dot(R, r, A.w[r], A.w), acc, 0, 0);
+  } else {
+    SubGrp<16> g;
+    const BlkParams P{};
+    const int gi = (((int)blockIdx.x - ga) * blockDim.x + threadIdx.x) >> 4;
+    const int gn = (((int)gridDim.x - ga) * blockDim.x) >> 4;
+    for (int i = gi; i < nb; i += gn) {
+      const PdcsBlock b = tab[i];
+      for (int q = g.rank; q < b.dim; q += g.size) {
+        const int r = b.start + q;
+        y_epilogue<false>(A, k, r, cls_dot(R, r, A.w[r], A.w), acc, 0, 0);
+      }
+      g.sync();
+      do_block<SubGrp<16>, OP_STEP_Y>(g, b, A, P, acc);
+    }
+    __syncwarp();
+  }
+  block_store_mask<GY_N>(acc, 0u, part, cap, blockIdx.x);
+}
+
 template <bool H>
 __global__ void __launch_bounds__(BS, 8) k_t_epi(KArgs A, double* part, int cap, CtrlFuse F, ShortRows R) {
   pdl_enter();

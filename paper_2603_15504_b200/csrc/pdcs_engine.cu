@@ -461,11 +461,12 @@ int launch_rowred(const SpmvPlan& P, const double* val, double* out, cudaStream_
 }
 
 // ---- cone block tables -------------------------------------------------------
-int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bool giant_ok = false) {
+int build_table(BlockTable& T, std::vector<PdcsBlock> blocks, cudaStream_t s, bool giant_ok = false,
+                int thread_max = THREAD_CLASS_MAX) {
   std::vector<PdcsBlock> ex, th, hf, wa, ct, gi;
   for (auto& b : blocks) {
     if ((b.kind == PDCS_EXP || b.kind == PDCS_DUAL_EXP) && b.dim == 3) ex.push_back(b);
-    else if (b.dim <= THREAD_CLASS_MAX) th.push_back(b);
+    else if (b.dim <= thread_max) th.push_back(b);
     else if (b.dim <= HALF_CLASS_MAX) hf.push_back(b);
     else if (b.dim <= WARP_CLASS_MAX) wa.push_back(b);
     else if (giant_ok && b.kind == PDCS_SOC && b.dim > GIANT_MIN) gi.push_back(b);
@@ -1230,7 +1231,16 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     pos += dim;
   }
   if (pos != d.m) { g_err = "pdcs_engine_create: dual cone dims do not sum to m"; return fail(2); }
-  if (build_table(E->tabX, xb, s) || build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc)) return fail(1);
+  // blocks up to thread_max rows get one thread each.  Dual blocks (uniformly scaled: plain
+  // SOC projections) up to 16 rows: a thread per block runs C2's 10k SOC(11) blocks in one
+  // wave (C2 +4% over 16-lane groups); primal blocks keep the 16-lane groups, whose rescaled-SOC
+  // root searches a lone thread would serialise (C2p 3.5k vs 5.3k it/s).  PDCS_TUNE
+  // thread_max=N / xthread_max=N override.
+  const int ythr = (int)tune_env("thread_max", d.allow_nonuniform_dual_soc ? (double)THREAD_CLASS_MAX : 16.0);
+  const int xthr = (int)tune_env("xthread_max", (double)THREAD_CLASS_MAX);
+  if (build_table(E->tabX, xb, s, false, xthr) ||
+      build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc, ythr))
+    return fail(1);
   E->xblocks = xb;
   E->has_xblocks = E->tabX.total() > 0;
   E->tabY.half_minb = (int)tune_env("halfminb", 3.0);

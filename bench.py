@@ -414,6 +414,7 @@ def run_ours(args, rank, world, local):
     # no per-stage profile (--profile-reps 0): no kernel roofline (null, not NaN)
     dom_gbs = dom_bytes / (dom[1] / 1000.0) / 1e9 if dom[1] else None
     slot_ms = sum(s[1] for s in stages)
+    loop.close()
     del loop
     torch.cuda.empty_cache()
 

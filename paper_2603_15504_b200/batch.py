@@ -144,4 +144,6 @@ def solve_many(problems, options: SolverOptions | None = None, max_workers: int 
             out = list(pool.map(member, range(len(loops))))
     finally:
         coord.close()
+        for lp in loops:
+            lp.close()
     return out

@@ -7,6 +7,7 @@ all arithmetic runs in libpdcs kernels (include/pdcs.h).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 
 import numpy as np
@@ -66,7 +67,8 @@ _stage_local = threading.local()
 # set by batch.solve_many's thread-pool path: engines built on this thread stay
 # on the CUDA-graph path (a persistent cooperative launch occupies the GPU)
 _thread_opts = threading.local()
-_COPY_THREADS = 4
+# host threads of the large staged copies (PDCS_COPY_THREADS overrides)
+_COPY_THREADS = max(1, int(os.environ.get("PDCS_COPY_THREADS", "4")))
 _copy_pool = None
 _copy_lock = threading.Lock()
 
@@ -342,7 +344,10 @@ class DeviceEngine:
                 N.check(lib.pdcs_engine_set_uniform_box(h, float(l0[0]), float(u0[0])),
                         "pdcs_engine_set_uniform_box")
 
-    def __del__(self):
+    def close(self):
+        """Destroy the libpdcs engine now (solve() calls this when it returns:
+        left to the garbage collector, the destroy -- pool frees and a stream
+        sync -- could land in the middle of the next solve's setup)."""
         h = getattr(self, "handle", None)
         if h is not None and h.value:
             try:
@@ -350,6 +355,9 @@ class DeviceEngine:
             except Exception:  # noqa: BLE001 - interpreter shutdown
                 pass
             self.handle = None
+
+    def __del__(self):
+        self.close()
 
     # -- thin wrappers ------------------------------------------------------
     def precondition(self, enabled: int, ruiz_iters: int = 10, use_pc: bool = True):

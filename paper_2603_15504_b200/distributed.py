@@ -356,4 +356,8 @@ def solve_sharded(problem: ConicProblem, options=None, group=None):
     options.validate()
     if not isinstance(problem, ConicProblem):
         problem = _adopt(problem)
-    return sharded_loop_class()(problem, options, group).run()
+    loop = sharded_loop_class()(problem, options, group)
+    try:
+        return loop.run()
+    finally:
+        loop.close()

@@ -713,7 +713,7 @@ int split_t(Engine* E, const KArgs& A) {
 template <int VW, int GP>
 int lane_y(Engine* E, const KArgs& A) {
   if (lane_passes<VW, GP>(E, E->G, E->PG, E->d.d_xt, E->d_wpart_y, 1, E->keep_xt)) return 1;
-  CK(launch_step(use_pdl(E), k_step_y_lane<VW, GP>, E->G.grid, E->stream, A, E->G.nrows,
+  CK(launch_step(use_pdl(E), k_step_y_lane<VW, GP>, E->G.grid, E->stream, A, E->exp_fused ? E->m_elem : E->G.nrows,
                  tile_source(E->G, E->PG, E->PG.np - 1, E->d_wpart_y), E->d_partY, E->capY, fuse_ls(E)));
   CKL();
   return 0;
@@ -981,7 +981,14 @@ int launch_slot(Engine* E) {
   mark(s, "step_y_spmv");
   // else projected inside the tiled y-step (soc_tile) or the class-split epilogue (yblk_fused)
   const bool yblk = E->has_yblocks && !E->soc_tile && !E->yblk_fused;
-  if (yblk && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s)) return 1;
+  if (E->exp_fused) {  // the exp rows' y-step inside the block kernel (k_exp_ystep)
+    const ShortRows R{E->G.rowptr, E->G.colidx, E->G.val, E->d.d_xt};
+    auto fn = E->tabY.exp_minb == 3 ? k_exp_ystep<3> : (E->tabY.exp_minb == 2 ? k_exp_ystep<2> : k_exp_ystep<4>);
+    fn<<<E->tabY.g_exp, BS, 0, s>>>(E->tabY.d_all, E->tabY.n_exp, A, R, E->d_partY, E->capY, E->G.grid);
+    CKL();
+  } else if (yblk && launch_blocks<OP_STEP_Y>(E->tabY, A, none, E->d_partY, E->capY, E->G.grid, 1, s)) {
+    return 1;
+  }
   if (yblk) mark(s, "blocks_y");
   if (E->comm) {
     // sharded: the five y-space and three x-space line-search sums over all
@@ -1466,6 +1473,15 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
         const int nx = grid_for(d.n, BS, 1 << 30);
         E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
                                                   : fit((const void*)k_t_epi<false>, nx));
+      }
+    }
+    // exp-cone rows' y-step in the exp block kernel (PDCS_TUNE expfuse=0 off): lane-mapped
+    // single-panel y-step, dual blocks all exponential, long rows only among the elementwise rows
+    {
+      const BlockTable& T = E->tabY;
+      if (tune("expfuse", 1.0) > 0.0 && !E->cls_y && !E->split && !E->tile_y && E->PG.np == 1 && T.n_exp > 0 &&
+          T.n_exp == T.total() && d.m_elem < d.m && !T.exp_split) {
+        E->exp_fused = true;
       }
     }
     // the partial-sum passes are latency bound (dependent rowptr -> col ->

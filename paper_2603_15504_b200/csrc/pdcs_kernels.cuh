@@ -1428,6 +1428,75 @@ __device__ __forceinline__ void cls_cone_cols(const KArgs& A, const ShortRows& R
     cls_dot(R, j, 0.0, A.gth);
 }
 
+// y-step of the exponential-cone rows in the block kernel itself (C3: 3M of
+// its 3.001M rows): each thread forms its block's three products of G^ x~
+// (index-order sums, as the lane kernels), the pending Halpern update and the
+// dual candidate of y_epilogue, then projects -- the rows' v, w and gx_hat
+// make no round trip through HBM and the step kernel only covers the
+// elementwise rows.  The same arithmetic as y_epilogue + k_blk_exp<OP_STEP_Y>.
+template <int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_exp_ystep(const PdcsBlock* tab, int nb, KArgs A, ShortRows R,
+                                                        double* part, int cap, int slot0) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ YCoef ks;
+  if (threadIdx.x == 0) ks = y_coef(C);
+  __syncthreads();
+  const YCoef& k = ks;
+  double acc[GY_N] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  int err = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const PdcsBlock b = tab[i];
+    const int s = b.start;
+    double v[3], o[3], res[3], rp[3], yn[3], dg[3], hv[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int r = s + q;
+      double d = 0.0;
+      for (int j = __ldg(R.rp + r), e = __ldg(R.rp + r + 1); j < e; ++j) d += __ldg(R.va + j) * R.x[__ldg(R.ci + j)];
+      double y0, g0;
+      if (k.pend) {
+        const double yo = A.y[r];
+        y0 = k.a * (k.opb * A.yh[r] - k.be * yo) + k.b * A.ya[r];
+        const double go = A.gx[r];
+        g0 = k.a * (k.opb * A.gxh[r] - k.be * go) + k.b * A.gxa[r];
+        A.yb[r] = (k.W == 0.0) ? y0 : (k.W * A.yb[r] + k.et * y0) / k.tot;
+        A.y[r] = y0;
+        A.gx[r] = g0;
+      } else {
+        y0 = A.y[r];
+        g0 = A.gx[r];
+      }
+      const double hi = A.h[r];
+      v[q] = y0 + k.sigma * (hi - d);
+      const double gh = 0.5 * (d + g0);
+      A.gxh[r] = gh;
+      A.w[r] = d;
+      res[q] = gh - hi;
+      yn[q] = y0;
+      dg[q] = d - g0;
+      hv[q] = hi;
+    }
+    double* rho = A.exp_rho ? A.exp_rho + 2 * (size_t)i : nullptr;  // warm starts
+    exp_or_dual(dual_kind(b.kind), v, o, &err, rho);
+    exp_or_dual(b.kind, res, rp, &err, rho ? rho + 1 : nullptr);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double p = o[q];
+      A.yh[s + q] = p;
+      const double dy = p - yn[q];
+      acc[GY_YY] += yn[q] * yn[q];
+      acc[GY_DYDY] += dy * dy;
+      acc[GY_INTER] += dy * dg[q];
+      const double viol = res[q] - rp[q];
+      acc[GY_RP2] += viol * viol;
+      acc[GY_YH] += p * hv[q];
+    }
+  }
+  if (err) set_err(A.err, err);
+  block_store_mask<GY_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
 // ---- 16-byte (double2) streaming variants of the step epilogues -------------
 // The same per-element arithmetic as k_step_x / y_epilogue / t_epilogue, with
 // every stream moved as aligned pairs (one 16-byte load or store per two

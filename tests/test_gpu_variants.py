@@ -62,6 +62,13 @@ def _exp():
     return instances.entropy_max(nblk=3000, p=40, nnz_per_col=3, seed=3)
 
 
+def _rsoc():
+    from paper_2603_15504_b200 import instances
+
+    # C4's structure: dense factor columns give G^T rows a leading run of consecutive columns
+    return instances.markowitz_rsoc(N=20_000, k=20, seed=4)
+
+
 def _lp():
     from paper_2603_15504_b200 import instances
 
@@ -83,6 +90,7 @@ CASES = [
     ("mixed", "cls_nnz=0,cls_frac=0,vec=0"),        # class split with scalar epilogues
     ("exp", ""),                         # exp rows' y-step inside the exp block kernel
     ("exp", "expfuse=0"),                # lane y-step over all rows + k_blk_exp
+    ("rsoc", "cls_nnz=0"),                # class split of G^T rows of one length (C4's structure)
     ("lp", "py=3,pt=2,split=1"),         # column panels: gather-only passes + streaming epilogues
     ("lp", "py=3,pt=2,split=0"),         # column panels, fused step kernels
     ("lp", "py=3,pt=2,split=1,hs=0,vec=0"),  # split without L2 hints / double2 epilogues
@@ -95,7 +103,8 @@ CASES = [
 def test_variant_trajectory_matches_oracle(shape, tune, monkeypatch):
     import paper_2603_15504_b200 as P
 
-    p = {"mixed": _mixed, "lp": _lp, "primal_soc": _primal_soc, "primal_exp": _primal_exp, "exp": _exp}[shape]()
+    p = {"mixed": _mixed, "lp": _lp, "primal_soc": _primal_soc, "primal_exp": _primal_exp, "exp": _exp,
+         "rsoc": _rsoc}[shape]()
     kb = (1, 2, 5, 10)
     dev, orc = _trajectory(P, p, dict(max_iter=10, rel_tol=1e-14, abs_tol=1e-14), kb, tune, monkeypatch)
     assert sorted(dev) == sorted(orc) and dev, (sorted(dev), sorted(orc))

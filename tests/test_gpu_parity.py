@@ -290,6 +290,34 @@ def test_full_size_c5_spmv_is_bit_identical_to_scipy(P):
     assert abs(float(y @ gx) - float(gty @ x)) <= 1e-9 * abs(float(y @ gx))
 
 
+def test_full_size_c5_step_spmvs_are_bit_identical_to_scipy(P):
+    """The panelled step SpMVs of the solve loop itself (C5: 3 column panels of
+    G^, 2 of G^T, gather-only passes carrying each row's partial sum, then the
+    streaming epilogues): every row is still summed in index order, so after a
+    few PDHG trials w = G^ x~ and gth = G^T y_hat equal scipy's csr_matvec on
+    the device's own scaled matrix bit for bit."""
+    import scipy.sparse as sp
+
+    from paper_2603_15504_b200 import instances
+    from paper_2603_15504_b200.engine import _Loop
+
+    p = instances.lp_large()
+    loop = _Loop(p, P.SolverOptions(max_iter=3, rel_tol=1e-14, abs_tol=1e-14))
+    try:
+        loop.run()
+        d = loop.dev
+        info = d.info()
+        assert info.get("panels_g", 1) > 1 and info.get("panels_gt", 1) > 1, info
+        m, n, nnz = d.m, d.n, d.nnz
+        G = sp.csr_matrix((d.host(d.g_val, nnz), d.host(d.g_colidx, nnz), d.host(d.g_rowptr, m + 1)),
+                          shape=(m, n))
+        np.testing.assert_array_equal(d.host(d.w, m), G @ d.host(d.xt, n))
+        if d.get_ctrl().accepted:  # gth belongs to the last accepted trial's y_hat
+            np.testing.assert_array_equal(d.host(d.gth, n), G.T.tocsr() @ d.host(d.yh, m))
+    finally:
+        loop.close()
+
+
 def test_solve_many_matches_sequential(P, monkeypatch):
     """Concurrent solves (one engine + stream per instance, host threads) give
     the bit-identical results of sequential solves."""

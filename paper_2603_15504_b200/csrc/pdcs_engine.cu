@@ -952,10 +952,15 @@ int launch_slot(Engine* E) {
   BlkParams none{nullptr, nullptr, nullptr, 0, -1};
   // primal candidate (pairs of coordinates per 16-byte access when the whole
   // x-space is one uniform box on one GPU)
-  if (E->vec && E->ubox && E->nbox == E->n && !E->comm && !E->xsplit)
+  if (E->vec && E->ubox && E->nbox == E->n && !E->comm && !E->xsplit) {
     CK(launch_step(use_pdl(E), k_step_x2, E->gridStepX2, s, A, E->d_partX, E->capX));
-  else
+  } else if (E->xexp_fused) {  // the cone coordinates are stepped by k_exp_xstep
+    KArgs Ab = A;
+    Ab.x1 = std::min(A.x1, E->nbox);
+    CK(launch_step(use_pdl(E), k_step_x<false>, E->gridStepX, s, Ab, E->d_partX, E->capX));
+  } else {
     CK(launch_step(use_pdl(E), k_step_x<false>, E->gridStepX, s, A, E->d_partX, E->capX));
+  }
   CKL();
   mark(s, "step_x");
   // x-space cone blocks this engine steps (its slice's blocks when sharded)
@@ -965,7 +970,12 @@ int launch_slot(Engine* E) {
     g_err = "sharded engine: pdcs_engine_set_xsplit is required with more than one rank";
     return 2;
   }
-  if (xblk && launch_blocks<OP_STEP_X>(TX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s)) return 1;
+  if (E->xexp_fused) {
+    k_exp_xstep<4><<<TX.g_exp, BS, 0, s>>>(TX.d_all, TX.n_exp, A, E->d_partX, E->capX, E->gridStepX);
+    CKL();
+  } else if (xblk && launch_blocks<OP_STEP_X>(TX, A, none, E->d_partX, E->capX, E->gridStepX, 1, s)) {
+    return 1;
+  }
   if (xblk) mark(s, "blocks_x");
   if (E->comm) {
     // sharded: every rank stepped its x-slice; G_p x~ needs all of x~
@@ -1474,6 +1484,12 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
         E->GT.grid = grid_per_sm("gt", nx, E->vec ? fit((const void*)k_t_epi2, nx)
                                                   : fit((const void*)k_t_epi<false>, nx));
       }
+    }
+    // primal exp coordinates' x-step in the exp block kernel (PDCS_TUNE xexpfuse=0 off):
+    // every primal block exponential (single GPU: the sharded x-slice tables differ)
+    {
+      const BlockTable& T = E->tabX;
+      E->xexp_fused = tune("xexpfuse", 1.0) > 0.0 && T.n_exp > 0 && T.n_exp == T.total();
     }
     // exp-cone rows' y-step in the exp block kernel (PDCS_TUNE expfuse=0 off): lane-mapped
     // single-panel y-step, dual blocks all exponential, long rows only among the elementwise rows

@@ -1428,6 +1428,70 @@ __device__ __forceinline__ void cls_cone_cols(const KArgs& A, const ShortRows& R
     cls_dot(R, j, 0.0, A.gth);
 }
 
+// x-step of the primal exponential-cone coordinates in the block kernel itself
+// (C3p: all 3M of its coordinates): each thread applies the pending Halpern
+// update and forms the candidate v = x - tau (c - G^T y) of its block's three
+// coordinates, then projects -- v makes no round trip through HBM and the
+// x-step kernel only covers the box.  The same arithmetic as k_step_x +
+// k_blk_exp<OP_STEP_X>.
+template <int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_exp_xstep(const PdcsBlock* tab, int nb, KArgs A, double* part,
+                                                        int cap, int slot0) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop) return;
+  __shared__ double kc[8];
+  if (threadIdx.x == 0) {
+    kc[0] = C->pa; kc[1] = C->pb; kc[2] = C->pbeta; kc[3] = C->peta; kc[4] = C->pW; kc[5] = C->tau;
+    kc[6] = 1.0 + C->pbeta; kc[7] = C->pW + C->peta;
+  }
+  __syncthreads();
+  const double &a = kc[0], &b = kc[1], &be = kc[2], &et = kc[3], &W = kc[4], &tau = kc[5];
+  const double &opb = kc[6], &tot = kc[7];
+  const bool pend = C->pending != 0;
+  double acc[GX_N] = {0.0, 0.0, 0.0};
+  int err = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const PdcsBlock bk = tab[i];
+    const int s = bk.start;
+    double v[3], o[3], xv[3], cv[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int j = s + q;
+      double xn, gn;
+      if (pend) {
+        const double xo = A.x[j];
+        xn = a * (opb * A.xh[j] - be * xo) + b * A.xa[j];
+        const double go = A.gty[j];
+        gn = a * (opb * A.gth[j] - be * go) + b * A.gtya[j];
+        A.xb[j] = (W == 0.0) ? xn : (W * A.xb[j] + et * xn) / tot;
+        A.x[j] = xn;
+        A.gty[j] = gn;
+      } else {
+        xn = A.x[j];
+        gn = A.gty[j];
+      }
+      const double cj = A.c[j];
+      v[q] = xn - tau * (cj - gn);
+      xv[q] = xn;
+      cv[q] = cj;
+    }
+    exp_or_dual(bk.kind, v, o, &err);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int j = s + q;
+      const double p = o[q];
+      A.xh[j] = p;
+      A.xt[j] = 2.0 * p - xv[q];
+      const double d = p - xv[q];
+      acc[GX_XX] += xv[q] * xv[q];
+      acc[GX_DXDX] += d * d;
+      acc[GX_CX] += cv[q] * p;
+    }
+  }
+  if (err) set_err(A.err, err);
+  block_store_mask<GX_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
 // y-step of the exponential-cone rows in the block kernel itself (C3: 3M of
 // its 3.001M rows): each thread forms its block's three products of G^ x~
 // (index-order sums, as the lane kernels), the pending Halpern update and the

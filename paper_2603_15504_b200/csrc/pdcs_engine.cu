@@ -722,7 +722,7 @@ int lane_y(Engine* E, const KArgs& A) {
 template <int VW, int GP>
 int lane_t(Engine* E, const KArgs& A) {
   if (lane_passes<VW, GP>(E, E->GT, E->PGT, E->d.d_yh, E->d_wpart_x, 2, E->keep_yh)) return 1;
-  CK(launch_step(use_pdl(E), k_step_t_lane<VW, GP>, E->GT.grid, E->stream, A, E->GT.nrows,
+  CK(launch_step(use_pdl(E), k_step_t_lane<VW, GP>, E->GT.grid, E->stream, A, (E->texp_fused && !E->comm) ? E->nbox : E->GT.nrows,
                  tile_source(E->GT, E->PGT, E->PGT.np - 1, E->d_wpart_x), E->d_partT, E->capT,
                  fuse_beta(E)));
   CKL();
@@ -1035,7 +1035,13 @@ int launch_slot(Engine* E) {
     if (rc) return 1;
     mark(s, "step_t_spmv");
   }
-  if (xblk && launch_blocks<OP_TLAM>(TX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s)) return 1;
+  if (E->texp_fused && !E->comm) {  // sharded: G^T y_hat comes from the reduce-scatter
+    const ShortRows R{E->GT.rowptr, E->GT.colidx, E->GT.val, E->d.d_yh};
+    k_exp_tstep<4><<<TX.g_exp, BS, 0, s>>>(TX.d_all, TX.n_exp, A, R, E->d_partT, E->capT, E->GT.grid);
+    CKL();
+  } else if (xblk && launch_blocks<OP_TLAM>(TX, A, none, E->d_partT, E->capT, E->GT.grid, 2, s)) {
+    return 1;
+  }
   if (xblk) mark(s, "blocks_t");
   const double* tred = nullptr;
   if (E->comm) {
@@ -1490,6 +1496,9 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     {
       const BlockTable& T = E->tabX;
       E->xexp_fused = tune("xexpfuse", 1.0) > 0.0 && T.n_exp > 0 && T.n_exp == T.total();
+      // ... and their G^T rows + lambda_2 projection (lane-mapped single-panel t-step)
+      E->texp_fused = E->xexp_fused && tune("texpfuse", 1.0) > 0.0 && !E->cls_t && !E->split && !E->tile_t &&
+                      E->PGT.np == 1 && E->GT.n_long == 0;
     }
     // exp-cone rows' y-step in the exp block kernel (PDCS_TUNE expfuse=0 off): lane-mapped
     // single-panel y-step, dual blocks all exponential, long rows only among the elementwise rows

@@ -138,6 +138,7 @@ struct Engine {
   bool vec = false;       // 16-byte streaming epilogues of the split step
   bool cls_y = false, cls_t = false;
   bool xexp_fused = false;  // primal exp coordinates' x-step inside the exp block kernel (k_exp_xstep)
+  bool texp_fused = false;  // their G^T rows and lambda_2 projection in one kernel (k_exp_tstep)
   bool exp_fused = false;   // exp rows' y-step inside the exp block kernel (k_exp_ystep)
   bool yblk_fused = false;  // half-warp dual blocks projected in the class-split epilogue (k_y_epi_blk)
   int yblk_ga = 1;          // its CTAs for the elementwise rows (the rest take the blocks)  // class-split step SpMVs (mixed row lengths)

@@ -1492,6 +1492,42 @@ __global__ void __launch_bounds__(BS, MINB) k_exp_xstep(const PdcsBlock* tab, in
   block_store_mask<GX_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }
 
+// G^T y_hat rows of the primal exponential-cone coordinates and their
+// lambda_2 projection in one kernel (C3p): each thread sums its block's three
+// rows of G^T (index order, as the lane kernels), stores them in gth and
+// projects c - G^T y_hat onto the dual cone for beta's dual residual -- the
+// t-step kernel only covers the box.  The same arithmetic as the lane t-step
+// + k_blk_exp<OP_TLAM>.
+template <int MINB>
+__global__ void __launch_bounds__(BS, MINB) k_exp_tstep(const PdcsBlock* tab, int nb, KArgs A, ShortRows R,
+                                                        double* part, int cap, int slot0) {
+  const PdcsCtrl* C = A.ctrl;
+  if (C->stop || !C->accepted) return;
+  double acc[GT_N] = {0.0, 0.0, 0.0};
+  int err = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const PdcsBlock bk = tab[i];
+    const int s = bk.start;
+    double v[3], o[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int j = s + q;
+      double d = 0.0;
+      for (int k = __ldg(R.rp + j), e = __ldg(R.rp + j + 1); k < e; ++k) d += __ldg(R.va + k) * R.x[__ldg(R.ci + k)];
+      A.gth[j] = d;
+      v[q] = A.c[j] - d;
+    }
+    exp_or_dual(dual_kind(bk.kind), v, o, &err);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double dv = v[q] - o[q];
+      acc[GT_RD2] += dv * dv;
+    }
+  }
+  if (err) set_err(A.err, err);
+  block_store_mask<GT_N>(acc, 0u, part, cap, slot0 + blockIdx.x);
+}
+
 // y-step of the exponential-cone rows in the block kernel itself (C3: 3M of
 // its 3.001M rows): each thread forms its block's three products of G^ x~
 // (index-order sums, as the lane kernels), the pending Halpern update and the

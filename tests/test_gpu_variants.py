@@ -84,6 +84,7 @@ CASES = [
     ("primal_soc", "cls_nnz=0,cls_frac=0"),  # class split with primal cone columns after the box
     ("primal_exp", "cls_nnz=0,cls_frac=0"),
     ("primal_exp", "xexpfuse=0"),        # x-step kernel over all coordinates + k_blk_exp<OP_STEP_X>
+    ("primal_exp", "texpfuse=0"),        # fused x-step, lane t-step over all rows + k_blk_exp<OP_TLAM>
     ("primal_soc", "cls=0"),
     ("lp", "cls_nnz=0,cls_frac=0"),       # class split on uniform short rows (all in the epilogue)
     ("mixed", "cls=0,tile=1"),           # tiled step kernels forced

@@ -1658,12 +1658,20 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
   // rank ends with its slice of D1 and the global D2 (SURVEY 8(e) "At setup")
   const bool shard = E->comm && E->nranks > 1;
   if (enabled == 1 && (nnz > 0 || shard)) {
-    // Ruiz rounds on a working copy held in g_val (scaling.py:84-90)
-    if (nnz > 0)
+    // Ruiz rounds on working copies held in g_val and gt_val (scaling.py:84-90):
+    // both are scaled in place each round, G^T's entries with the operands of
+    // their G entries ((r_row * v) * c_col, the same operations, so gt_val stays
+    // the exact transpose of g_val) -- no random gather of g_val per round
+    int* rowid_t = nullptr;
+    if (nnz > 0) {
       CK(cudaMemcpyAsync(d.d_g_val, d.d_g_val0, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
-    for (int it = 0; it < ruiz_iters; ++it) {
       k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
       CKL();
+      CK(cudaMallocAsync(&rowid_t, sizeof(int) * nnz, s));
+      k_iota_rows<<<grid_for(n), BS, 0, s>>>(d.d_gt_rowptr, n, rowid_t);
+      CKL();
+    }
+    for (int it = 0; it < ruiz_iters; ++it) {
       if (launch_rowred<0>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
       if (launch_rowred<0>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
       if (shard && nccl_allreduce(d.d_tx0, d.d_tx0, n, E->comm, s, ncclMax)) return 1;
@@ -1674,11 +1682,13 @@ int pdcs_precondition(PdcsEngine* E, int32_t enabled, int32_t ruiz_iters, int32_
       k_scale_vals<<<grid_for(nnz), BS, 0, s>>>(d.d_g_val, d.d_g_val, rowid, d.d_g_colidx, d.d_ty1,
                                                 d.d_tx1, nnz);
       CKL();
-    }
-    T.lap("ruiz rounds");
-    if (use_pc) {  // Pock-Chambolle alpha = 1 (scaling.py:92-96)
-      k_gather<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_g_val, d.d_perm, nnz);
+      k_scale_vals<<<grid_for(nnz), BS, 0, s>>>(d.d_gt_val, d.d_gt_val, d.d_gt_colidx, rowid_t, d.d_ty1,
+                                                d.d_tx1, nnz);
       CKL();
+    }
+    if (rowid_t) CK(cudaFreeAsync(rowid_t, s));
+    T.lap("ruiz rounds");
+    if (use_pc) {  // Pock-Chambolle alpha = 1 (scaling.py:92-96); gt_val is g_val's transpose
       if (launch_rowred<1>(E->G, d.d_g_val, d.d_ty0, s)) return 1;
       if (launch_rowred<1>(E->GT, d.d_gt_val, d.d_tx0, s)) return 1;
       if (shard && nccl_allreduce(d.d_tx0, d.d_tx0, n, E->comm, s, ncclSum)) return 1;

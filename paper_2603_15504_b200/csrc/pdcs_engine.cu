@@ -134,7 +134,8 @@ int nccl_allreduce(const double* send, double* recv, size_t count, void* comm, c
 // all-gather / reduce-scatter on buffers padded to nranks * xcnt; slices cut
 // at primal cone-block boundaries use grouped per-root broadcasts / reduces.
 int nccl_x_allgather(const Engine* E, double* v, cudaStream_t s) {
-  if (E->nranks <= 1) return 0;
+  // no early exit at one rank: the (in-place, no-op) all-gather then runs in the
+  // world-1 sharded tests, so the captured NCCL call itself is exercised on the GPU
   ncclComm_t comm = (ncclComm_t)E->comm;
   if (E->xcnt > 0) {
     CKN(g_nccl.allGather(v + (size_t)E->rank * E->xcnt, v, E->xcnt, ncclDouble, comm, s));

@@ -1590,17 +1590,23 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
 
 void pdcs_engine_destroy(PdcsEngine* E) {
   if (!E) return;
+  PhaseTimer T("destroy", E->stream);
   if (E->stream) cudaStreamSynchronize(E->stream);
+  T.lap("stream drain");
   if (E->exec) cudaGraphExecDestroy(E->exec);
   if (E->graph) cudaGraphDestroy(E->graph);
+  T.lap("graph");
   free_plan(E->G);
   free_plan(E->GT);
+  T.lap("plans");
   free_panels(E->PG, E->stream);
   free_panels(E->PGT, E->stream);
   if (E->d_wpart_y) cudaFreeAsync(E->d_wpart_y, E->stream);
   if (E->d_wpart_x) cudaFreeAsync(E->d_wpart_x, E->stream);
   if (E->stream) cudaStreamSynchronize(E->stream);  // the stream may go away with the caller
+  T.lap("panels");
   if (E->comm && g_nccl.ok) g_nccl.commDestroy((ncclComm_t)E->comm);
+  T.lap("comm");
   cudaFree(E->d_yred);
   cudaFree(E->d_gtp);
   free_table(E->tabX);
@@ -1622,9 +1628,12 @@ void pdcs_engine_destroy(PdcsEngine* E) {
   cudaFree(E->d_out);
   cudaFree(E->d_err);
   cudaFree(E->d_ticket);
+  T.lap("device buffers");
   if (E->h_pinned) cudaFreeHost(E->h_pinned);
+  T.lap("pinned");
   for (cudaEvent_t ev : E->ev_ctrl)
     if (ev) cudaEventDestroy(ev);
+  T.lap("events");
   delete E;
 }
 

@@ -67,14 +67,16 @@ _stage_local = threading.local()
 # set by batch.solve_many's thread-pool path: engines built on this thread stay
 # on the CUDA-graph path (a persistent cooperative launch occupies the GPU)
 _thread_opts = threading.local()
-# host threads of the large staged copies (PDCS_COPY_THREADS overrides)
-_COPY_THREADS = max(1, int(os.environ.get("PDCS_COPY_THREADS", "4")))
+# host threads of the large staged copies (PDCS_COPY_THREADS overrides): copies
+# into freshly allocated result arrays are page-fault bound (one thread: 5 GB/s,
+# four: 18 GB/s; tools/host_copy_probe.py); 8 took C5's download 36-40 -> 30-34 ms
+_COPY_THREADS = max(1, int(os.environ.get("PDCS_COPY_THREADS", str(min(8, os.cpu_count() or 4)))))
 _copy_pool = None
 _copy_lock = threading.Lock()
 
 
 def _pcopy(dst: np.ndarray, src: np.ndarray) -> None:
-    """dst[:] = src (flat uint8 views) with up to 4 host threads (numpy
+    """dst[:] = src (flat uint8 views) with up to _COPY_THREADS host threads (numpy
     releases the GIL in the copy): ~19 GB/s into pinned memory instead of
     ~8.5 on one thread, the host side of every large upload / download."""
     global _copy_pool

@@ -41,6 +41,7 @@ def main(reps):
     timed(device.DeviceEngine, "run_inner", "run_inner")
     timed(engine._Loop, "__init__", "loop init")
     timed(engine._Loop, "run", "loop run")
+    timed(engine._Loop, "close", "close")
     _, make = bench.WORKLOADS["C5"]
     p = make(instances)
     opts = SolverOptions(rel_tol=1e-12, abs_tol=1e-12, max_iter=20, time_limit=1e9)

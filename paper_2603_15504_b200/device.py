@@ -62,7 +62,8 @@ def _slab(dtype, sizes: dict, align: int = 64) -> dict:
     return {name: buf[off:off + max(int(sizes[name]), 1)] for name, off in offs.items()}
 
 
-_STAGE_BYTES = 32 << 20
+_STAGE_BYTES = int(os.environ.get("PDCS_STAGE_MB", "32")) << 20
+_NSTAGE = max(2, int(os.environ.get("PDCS_STAGES", "2")))  # pinned buffers per thread (upload pipeline depth)
 _stage_local = threading.local()
 # set by batch.solve_many's thread-pool path: engines built on this thread stay
 # on the CUDA-graph path (a persistent cooperative launch occupies the GPU)
@@ -106,7 +107,7 @@ def _stages():
     bufs = getattr(_stage_local, "bufs", None)
     if bufs is None:
         torch = _torch()
-        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(_NSTAGE)]
         _stage_local.bufs = bufs
     return bufs
 
@@ -127,10 +128,10 @@ def h2d(dst, arr, stream) -> None:
     src = a.view(np.uint8)
     dbytes = dst[: a.size].view(torch.uint8)
     st = _stages()
-    done = [None, None]
+    done = [None] * len(st)
     with torch.cuda.stream(stream):
         for i, off in enumerate(range(0, src.size, _STAGE_BYTES)):
-            b = i & 1
+            b = i % len(st)
             if done[b] is not None:
                 done[b].synchronize()
             k = min(_STAGE_BYTES, src.size - off)

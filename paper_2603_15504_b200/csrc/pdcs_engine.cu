@@ -547,7 +547,17 @@ int launch_blocks(const BlockTable& T, const KArgs& A, const BlkParams& P, doubl
   if (T.n_half) {
     // register budget of the step half-warp blocks: 3 CTAs per SM (80 registers)
     // measured best on C2 (PDCS_TUNE halfminb=1|3|4; profiles/r02_sweeps.txt)
-    if (OP != OP_PROJECT && T.half_minb == 4)
+    // lanes per block: 4 (default; fewer CTAs than the class's slots), 8, 2 or 16
+    if (OP != OP_PROJECT && T.half_w == 4)
+      k_blk_half<OP, 3, 4><<<std::min(T.g_half, grid_for(T.n_half, BS / 4)), BS, 0, s>>>(base, T.n_half, A, P,
+                                                                                         part, cap, slot, gate);
+    else if (OP != OP_PROJECT && T.half_w == 8)
+      k_blk_half<OP, 3, 8><<<std::min(T.g_half, grid_for(T.n_half, BS / 8)), BS, 0, s>>>(base, T.n_half, A, P,
+                                                                                         part, cap, slot, gate);
+    else if (OP != OP_PROJECT && T.half_w == 2)
+      k_blk_half<OP, 3, 2><<<std::min(T.g_half, grid_for(T.n_half, BS / 2)), BS, 0, s>>>(base, T.n_half, A, P,
+                                                                                         part, cap, slot, gate);
+    else if (OP != OP_PROJECT && T.half_minb == 4)
       k_blk_half<OP, 4><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
     else if (OP != OP_PROJECT && T.half_minb == 3)
       k_blk_half<OP, 3><<<T.g_half, BS, 0, s>>>(base, T.n_half, A, P, part, cap, slot, gate);
@@ -1255,12 +1265,10 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
     pos += dim;
   }
   if (pos != d.m) { g_err = "pdcs_engine_create: dual cone dims do not sum to m"; return fail(2); }
-  // blocks up to thread_max rows get one thread each.  Dual blocks (uniformly scaled: plain
-  // SOC projections) up to 16 rows: a thread per block runs C2's 10k SOC(11) blocks in one
-  // wave (C2 +4% over 16-lane groups); primal blocks keep the 16-lane groups, whose rescaled-SOC
-  // root searches a lone thread would serialise (C2p 3.5k vs 5.3k it/s).  PDCS_TUNE
-  // thread_max=N / xthread_max=N override.
-  const int ythr = (int)tune_env("thread_max", d.allow_nonuniform_dual_soc ? (double)THREAD_CLASS_MAX : 16.0);
+  // blocks up to thread_max rows (default 4) get one thread each, the next class 4-lane
+  // groups (half_w): measured better than a thread per SOC(11) block (C2 10.1k, C2p 3.5k it/s)
+  // and than 16-lane groups.  PDCS_TUNE thread_max=N / xthread_max=N override.
+  const int ythr = (int)tune_env("thread_max", (double)THREAD_CLASS_MAX);
   const int xthr = (int)tune_env("xthread_max", (double)THREAD_CLASS_MAX);
   if (build_table(E->tabX, xb, s, false, xthr) ||
       build_table(E->tabY, yb, s, !d.allow_nonuniform_dual_soc, ythr))
@@ -1269,6 +1277,10 @@ int pdcs_engine_create(const PdcsEngineDesc* desc, void* stream, PdcsEngine** ou
   E->has_xblocks = E->tabX.total() > 0;
   E->tabY.half_minb = (int)tune_env("halfminb", 3.0);
   E->tabX.half_minb = (int)tune_env("xhalfminb", 3.0);
+  // 4 lanes per block of 5-16 rows: C2 10.6k it/s vs 10.1k (a thread per block) and 9.7k
+  // (16 lanes); C2p 5.9k vs 5.3k (profiles/r02_sweeps.txt)
+  E->tabY.half_w = (int)tune_env("halfw", 4.0);
+  E->tabX.half_w = (int)tune_env("xhalfw", 4.0);
   if (E->tabY.n_exp) {  // Newton warm starts of the dual exp blocks, NaN = cold
     const size_t cnt = 2 * (size_t)E->tabY.n_exp;
     if (cudaMalloc(&E->d_exp_rho, sizeof(double) * cnt) != cudaSuccess) return fail(1);

@@ -70,6 +70,7 @@ struct BlockTable {
   // needing the root search at d_queue[c*exp_per ...], d_qcount[c] of them
   bool exp_split = false;
   int exp_per = 0;
+  int half_w = 16;    // lanes per block of the half-warp class kernel (PDCS_TUNE halfw / xhalfw = 4)
   int half_minb = 1;  // CTAs per SM the y-step half-warp block kernel is compiled for (PDCS_TUNE halfminb)
   int exp_minb = 4;  // CTAs per SM the exp kernels are compiled for (register budget; PDCS_TUNE expminb)
   int* d_queue = nullptr;   // [n_exp]

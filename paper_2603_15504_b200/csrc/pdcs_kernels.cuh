@@ -786,7 +786,8 @@ __global__ void __launch_bounds__(BS) k_blk_thread(const PdcsBlock* tab, int nb,
 
 // Small blocks (THREAD_CLASS_MAX < dim <= HALF_CLASS_MAX): 16 lanes per
 // block, two blocks per warp.
-template <int OP, int MINB = 1>
+// W lanes per block (16, or 4: shorter reductions, several rows per lane)
+template <int OP, int MINB = 1, int W = 16>
 __global__ void __launch_bounds__(BS, MINB) k_blk_half(const PdcsBlock* tab, int nb, KArgs A,
                                                  BlkParams P, double* part, int cap, int slot0,
                                                  int gate) {
@@ -795,10 +796,10 @@ __global__ void __launch_bounds__(BS, MINB) k_blk_half(const PdcsBlock* tab, int
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-  SubGrp<16> g;
-  const int gi = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;
-  const int gn = (gridDim.x * blockDim.x) >> 4;
-  for (int i = gi; i < nb; i += gn) do_block<SubGrp<16>, OP>(g, tab[i], A, P, acc);
+  SubGrp<W> g;
+  const int gi = (blockIdx.x * blockDim.x + threadIdx.x) / W;
+  const int gn = (gridDim.x * blockDim.x) / W;
+  for (int i = gi; i < nb; i += gn) do_block<SubGrp<W>, OP>(g, tab[i], A, P, acc);
   __syncwarp();
   if (OP != OP_PROJECT) block_store_mask<NQ>(acc, 0u, part, cap, slot0 + blockIdx.x);
 }

@@ -77,8 +77,11 @@ def _lp():
 
 CASES = [
     ("mixed", "cls_nnz=0,cls_frac=0"),   # class split: short rows thread/row, long rows 8/32 lanes
-    ("mixed", "cls_nnz=0,cls_frac=0,yblkfuse=1,thread_max=4"),  # class split, SOC blocks inside the epilogue
-    ("mixed", "thread_max=4"),           # dual SOC(11) blocks on 16-lane groups
+    ("mixed", "cls_nnz=0,cls_frac=0,yblkfuse=1"),  # class split, SOC blocks inside the epilogue
+    ("mixed", "halfw=16"),               # dual SOC(11) blocks on 16-lane groups (default 4)
+    ("mixed", "thread_max=16"),          # ... a thread per block
+    ("mixed", "halfw=8"),
+    ("primal_soc", "xhalfw=16"),         # primal rescaled SOC blocks on 16-lane groups
     ("mixed", "cls=0"),                  # tiled / 8-lane step kernels
     ("mixed", "cls_nnz=0,cls_frac=0,cls_vw=32"),    # class split, 32 lanes per long row
     ("primal_soc", "cls_nnz=0,cls_frac=0"),  # class split with primal cone columns after the box

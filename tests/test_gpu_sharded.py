@@ -92,3 +92,40 @@ def test_sharded_trajectory_close_to_single_gpu(group):
     for kb in (10, 20):
         for a, b in zip(snaps["one"][kb], snaps["sharded"][kb]):
             assert np.max(np.abs(a - b)) <= 1e-11 * max(1.0, float(np.max(np.abs(a))))
+
+
+@pytest.mark.parametrize("shape,tune", [("mixed", "cls_nnz=0,cls_frac=0"), ("exp", ""), ("primal_exp", ""),
+                                        ("primal_soc", "cls_nnz=0,cls_frac=0"), ("lp", "py=3,pt=2")])
+def test_sharded_launch_variants_track_single_gpu(group, shape, tune, monkeypatch):
+    """The sharded engine (world of one) with the single-GPU launch variants
+    active -- class-split steps, exp steps fused into the block kernels,
+    4-lane cone groups, column panels -- follows the single-GPU trajectory."""
+    import paper_2603_15504_b200 as P
+    from paper_2603_15504_b200 import instances
+    from paper_2603_15504_b200.distributed import solve_sharded
+
+    p = {"mixed": lambda: instances.group_robust_regression(ngroups=300, gsize=10, q=400, nnz_per_row=40, seed=5),
+         "exp": lambda: instances.entropy_max(nblk=3000, p=40, nnz_per_col=3, seed=3),
+         "primal_exp": lambda: instances.entropy_max_primal(nblk=3000, p=40, nnz_per_col=3, seed=3),
+         "primal_soc": lambda: instances.group_regression_primal(ngroups=200, gsize=10, q=300, nnz_per_row=30,
+                                                                 seed=4),
+         "lp": lambda: instances.lp_large(m=20_000, n=40_000, nnz_per_row=5, eq_frac=0.3, seed=2)}[shape]()
+    snaps = {"one": {}, "sharded": {}}
+
+    def grab(which):
+        def cb(s):
+            if s.k_bar in (5, 10):
+                snaps[which][s.k_bar] = (s.z.x.copy(), s.z.y.copy())
+        return cb
+
+    monkeypatch.setenv("PDCS_TUNE", tune)
+    try:
+        o = dict(max_iter=10, rel_tol=1e-14, abs_tol=1e-14)
+        P.solve(p, P.SolverOptions(**o, iteration_callback=grab("one")))
+        solve_sharded(p, P.SolverOptions(**o, iteration_callback=grab("sharded")))
+    finally:
+        monkeypatch.delenv("PDCS_TUNE")
+    assert sorted(snaps["one"]) == sorted(snaps["sharded"]) == [5, 10]
+    for kb in (5, 10):
+        for a, b in zip(snaps["one"][kb], snaps["sharded"][kb]):
+            assert np.max(np.abs(a - b)) <= 1e-10 * max(1.0, float(np.max(np.abs(a)))), (shape, kb)
